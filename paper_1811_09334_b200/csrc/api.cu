@@ -1,0 +1,789 @@
+// api.cu -- the C ABI of librqlp.so (include/rqlp.h): handles, workspace, argument checking and
+// the host orchestration of RQLP (Alg. 1), ERQLP (Alg. 2) and BRQLP (Alg. 3).  Every step of
+// the method runs in this library's kernels on the handle's stream; the host only enqueues.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "internal.cuh"
+
+struct rqlp_handle_s {
+  int magic = 0x51504c52;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  void *comm = nullptr;
+  int rank = 0, nranks = 1;
+  void *ws = nullptr;  // caller-provided
+  size_t ws_bytes = 0;
+  void *own = nullptr;  // library-owned (rqlp() / stage entry points without a workspace)
+  size_t own_bytes = 0;
+  unsigned *dflags = nullptr;
+  int64_t launches = 0;
+  bool timing = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> events;
+  std::vector<std::string> names_out;
+  std::vector<float> ms_out;
+  // staging buffers for host pointers in rqlp()
+  void *stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+namespace rqlpk {
+
+void launch_reduce(Ctx &c, int64_t M, int64_t N, int S, const double *part, double alpha, double beta, double *C,
+                   int64_t ldc, bool trans, const unsigned *cond, unsigned cond_mask);
+void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                     int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc, double *partials,
+                     size_t partial_elems, bool trans_out, const unsigned *cond, unsigned cond_mask);
+
+void Ctx::mark(const char *name) {
+  if (!timing || !events) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, stream);
+  events->emplace_back(name, e);
+}
+
+namespace {
+
+bool valid(rqlp_handle_t h) { return h && h->magic == 0x51504c52; }
+
+Ctx make_ctx(rqlp_handle_t h) {
+  Ctx c;
+  c.stream = h->stream;
+  c.device = h->device;
+  c.num_sms = h->num_sms;
+  c.dflags = h->dflags;
+  c.timing = h->timing;
+  c.events = &h->events;
+  c.comm = h->comm;
+  c.rank = h->rank;
+  c.nranks = h->nranks;
+  return c;
+}
+
+void reset_timing(rqlp_handle_t h) {
+  for (auto &e : h->events) cudaEventDestroy(e.second);
+  h->events.clear();
+}
+
+// ---- workspace plans ----------------------------------------------------------------------
+struct Plan {
+  int64_t m, n, l, ldm, ldn, ldl;
+  double *Om, *Y, *V, *Z, *W, *B, *QB, *T, *PB, *part;
+  size_t part_elems;
+  OrthScratch orth;
+  TailScratch tail;
+  // BRQLP extras
+  double *C, *D, *Qt2;
+};
+
+void carve_plan(Arena &a, Plan &p, int variant, int64_t m, int64_t n, int64_t l, int b, int num_sms) {
+  p.m = m; p.n = n; p.l = l;
+  p.ldm = round_up(m, 8); p.ldn = round_up(n, 8); p.ldl = round_up(l, 8);
+  int64_t lb = variant == RQLP_VARIANT_BRQLP ? b : l;  // block width of the passes
+  p.Om = a.take<double>(p.ldn * l);
+  p.Y = a.take<double>(p.ldm * l);
+  p.V = a.take<double>(p.ldm * l);
+  p.Z = a.take<double>(p.ldn * lb);
+  p.W = a.take<double>(p.ldn * lb);
+  p.B = a.take<double>(p.ldl * n);
+  p.QB = a.take<double>(p.ldl * l);
+  p.T = a.take<double>(p.ldl * l);
+  p.PB = a.take<double>(p.ldn * l);
+  p.part_elems = std::max(gemm_partials_needed(m, l, n, num_sms), gemm_partials_needed(n, l, m, num_sms));
+  p.part = a.take<double>((int64_t)p.part_elems);
+  orth_carve(a, p.orth, std::max(m, n), lb, num_sms);
+  tail_carve(a, p.tail, lb, n, num_sms);
+  if (variant == RQLP_VARIANT_BRQLP) {
+    p.C = a.take<double>(round_up(l, 8) * b);
+    p.D = a.take<double>(round_up(l, 8) * b);
+    p.Qt2 = a.take<double>(p.ldm * b);
+  } else {
+    p.C = p.D = p.Qt2 = nullptr;
+  }
+}
+
+size_t plan_bytes(int variant, int64_t m, int64_t n, int64_t l, int b, int num_sms) {
+  Arena a;
+  Plan p;
+  carve_plan(a, p, variant, m, n, l, b, num_sms);
+  return a.used + 4096;
+}
+
+// Workspace for a call: the caller's if set and large enough, else a library-owned buffer.
+char *get_ws(rqlp_handle_t h, size_t need, bool allow_own) {
+  if (h->ws) {
+    if (h->ws_bytes < need) throw std::runtime_error("workspace too small");
+    return (char *)h->ws;
+  }
+  if (!allow_own) throw std::runtime_error("no workspace");
+  if (h->own_bytes < need) {
+    if (h->own) cudaFree(h->own);
+    h->own = nullptr;
+    h->own_bytes = 0;
+    RQLP_CUDA(cudaMalloc(&h->own, need));
+    h->own_bytes = need;
+  }
+  return (char *)h->own;
+}
+
+struct WsError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int guarded(rqlp_handle_t h, F f) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  int rc = RQLP_OK;
+  try {
+    rc = f();
+  } catch (const CudaError &e) {
+    fprintf(stderr, "[rqlp] CUDA error: %s\n", e.what());
+    rc = RQLP_ERR_CUDA;
+  } catch (const std::exception &e) {
+    std::string w = e.what();
+    if (w.find("workspace") != std::string::npos) rc = RQLP_ERR_WORKSPACE;
+    else if (w.find("nccl") != std::string::npos || w.find("NCCL") != std::string::npos) rc = RQLP_ERR_NCCL;
+    else rc = RQLP_ERR_INTERNAL;
+    fprintf(stderr, "[rqlp] error: %s\n", e.what());
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return rc;
+}
+
+// Global row count for the l <= min(m, n) check on sharded handles is validated by the caller;
+// locally we require l <= n and m >= 1.
+int check_common(int64_t m, int64_t n, int k, int p, int q) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (k < 2) return -3;
+  if (p < 2) return -4;
+  if ((int64_t)k + p > n) return -3;
+  if (q < 0) return -5;
+  return 0;
+}
+
+// ---- RQLP / ERQLP ------------------------------------------------------------------------
+// Range finder + q subspace iterations (Alg.1 l.1-3 + reading R12), B = V^T A (Alg.1 l.4).
+void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, const double *A, int64_t lda,
+                       uint64_t seed) {
+  const bool sh = c.nranks > 1;
+  c.mark("start");
+  launch_omega(c, n, l, 0, seed, P.Om, P.ldn);                                        // l.1
+  c.mark("omega");
+  gemm_nn(c, m, l, n, A, lda, P.Om, P.ldn, P.Y, P.ldm, P.part, P.part_elems);         // l.2 Y = AΩ
+  c.mark("pass_sketch");
+  orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh);                      // l.3 V = qr(Y)
+  c.mark("orth");
+  for (int it = 0; it < q; ++it) {
+    gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.Z, P.ldn, false, P.part, P.part_elems); // Z = A^T V
+    allreduce_sum(c, P.Z, P.ldn * l);
+    c.mark("pass_power_AtV");
+    orth(c, P.orth, n, l, P.Z, P.ldn, P.W, P.ldn, nullptr, 0, false);                 // W = qr(Z)
+    c.mark("orth");
+    gemm_nn(c, m, l, n, A, lda, P.W, P.ldn, P.Y, P.ldm, P.part, P.part_elems);        // Y = A W
+    c.mark("pass_power_AW");
+    orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh);                    // V = qr(Y)
+    c.mark("orth");
+  }
+  gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.B, P.ldl, true, P.part, P.part_elems);    // l.4 B = V^T A
+  allreduce_sum(c, P.B, P.ldl * n);
+  c.mark("pass_project");
+}
+
+int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, const double *A, int64_t lda,
+             uint64_t seed, double *Q, int64_t ldq, double *T, int64_t ldt, double *Pout, int64_t ldp, int64_t *piv0,
+             int64_t *piv1, bool allow_own) {
+  int64_t l = (int64_t)k + p;
+  Ctx c = make_ctx(h);
+  reset_timing(h);
+  size_t need = plan_bytes(d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP, m, n, l, 0, c.num_sms);
+  Arena a;
+  a.base = get_ws(h, need, allow_own);
+  a.cap = need;
+  Plan P;
+  carve_plan(a, P, d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP, m, n, l, 0, c.num_sms);
+  RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+  range_and_project(c, P, m, n, l, q, A, lda, seed);
+  qlp_tail(c, P.tail, l, n, P.B, P.ldl, d, P.QB, P.ldl, T, ldt, Pout, ldp, piv0, piv1);   // l.5-7
+  gemm_nn(c, m, l, l, P.V, P.ldm, P.QB, P.ldl, Q, ldq, P.part, P.part_elems);             // Q = V Q_B
+  c.mark("assemble_Q");
+  h->launches = c.launches;
+  return RQLP_OK;
+}
+
+// ---- BRQLP -------------------------------------------------------------------------------
+// Alg.3 with implicit deflation: A^(j-1) X = A X - V_<j (B_<j X), A^(j-1)^T V = A^T V - B_<j^T (V_<j^T V).
+int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A, int64_t lda,
+              uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout, int64_t ldp, int64_t *piv0,
+              int64_t *piv1, bool allow_own) {
+  int64_t l = (int64_t)k + p;
+  Ctx c = make_ctx(h);
+  reset_timing(h);
+  const bool sh = c.nranks > 1;
+  size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l, b, c.num_sms);
+  Arena a;
+  a.base = get_ws(h, need, allow_own);
+  a.cap = need;
+  Plan P;
+  carve_plan(a, P, RQLP_VARIANT_BRQLP, m, n, l, b, c.num_sms);
+  RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+  const int64_t ldm = P.ldm, ldn = P.ldn, LL = P.ldl;
+  c.mark("start");
+  launch_omega(c, n, l, 0, seed, P.Om, ldn);                                            // l.1
+  c.mark("omega");
+  gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);               // l.3 all Y_j = AΩ_j
+  c.mark("pass_sketch");
+  launch_fill(c, l, l, L, ldl, 0.0, 0.0);
+  const int64_t h_blocks = ceil_div(l, b);
+  double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
+  for (int64_t j = 0; j < h_blocks; ++j) {
+    const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
+    double *Vj = P.V + c0 * ldm;
+    // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
+    auto reorth = [&]() {
+      if (c0 == 0) return;
+      gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
+      allreduce_sum(c, P.C, LL * bj);
+      gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
+                      nullptr, 0);
+      launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
+      orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
+    };
+    orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
+    reorth();                                                                            // l.5
+    for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
+      gemm_tn(c, m, bj, n, A, lda, Vj, ldm, P.Z, ldn, false, P.part, P.part_elems);     // Z = A^T Vj
+      allreduce_sum(c, P.Z, ldn * bj);
+      if (c0 > 0) {
+        gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems); // C = V_<j^T Vj
+        allreduce_sum(c, P.C, LL * bj);
+        gemm_generic_ex(c, true, false, n, bj, c0, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems, false,
+                        nullptr, 0);                                                     // Z -= B_<j^T C
+      }
+      orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
+      gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
+      if (c0 > 0) {
+        gemm_generic_ex(c, false, false, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems, false,
+                        nullptr, 0);                                                     // D = B_<j W
+        gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part,
+                        P.part_elems, false, nullptr, 0);                                // Y -= V_<j D
+      }
+      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
+      reorth();
+    }
+    // l.6: B_j = Vj^T A^(j-1) = Vj^T A - (Vj^T V_<j) B_<j, formed in the tail's B buffer
+    double *Bj = P.tail.Bw;
+    const int64_t ldbj = P.tail.ldl;
+    gemm_tn(c, m, bj, n, A, lda, Vj, ldm, Bj, ldbj, true, P.part, P.part_elems);
+    allreduce_sum(c, Bj, ldbj * n);
+    if (c0 > 0) {
+      gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, LL, false, P.part, P.part_elems);    // E = Vj^T V_<j (bj x c0)
+      allreduce_sum(c, P.D, LL * c0);
+      gemm_generic_ex(c, false, false, bj, n, c0, -1.0, P.D, LL, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems, false,
+                      nullptr, 0);
+    }
+    launch_copy(c, bj, n, Bj, ldbj, B + c0, LL, false);   // keep B_j for the later blocks' deflation
+    c.mark("block_passes");
+    // l.8: [Q_B, L_j, P_B] = qlp(B_j) (overwrites the tail's copy)
+    qlp_tail(c, P.tail, bj, n, P.tail.Bw, P.tail.ldl, 0, P.QB, P.tail.ldl, L + c0 + c0 * ldl, ldl, Pout + c0 * ldp,
+             ldp, piv0 ? piv0 + c0 : nullptr, piv1 ? piv1 + c0 : nullptr);
+    // l.9: Q_j = V_j Q_B
+    gemm_nn(c, m, bj, bj, Vj, ldm, P.QB, P.tail.ldl, Q + c0 * ldq, ldq, P.part, P.part_elems);
+    c.mark("block_tail");
+  }
+  h->launches = c.launches;
+  return RQLP_OK;
+}
+
+}  // namespace
+}  // namespace rqlpk
+
+using namespace rqlpk;
+
+// ================================ C ABI ================================================
+extern "C" {
+
+int rqlp_create(rqlp_handle_t *out, int device, void *cuda_stream) {
+  if (!out) return -1;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return RQLP_ERR_CUDA;
+  if (device < 0 || device >= ndev) return -2;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return RQLP_ERR_CUDA;
+  if (prop.major != 10) return RQLP_ERR_DEVICE;
+  auto *h = new rqlp_handle_s();
+  h->device = device;
+  h->stream = (cudaStream_t)cuda_stream;
+  h->num_sms = prop.multiProcessorCount;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaMalloc(&h->dflags, NUM_DEV_FLAGS * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(h->dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned));
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    delete h;
+    return RQLP_ERR_CUDA;
+  }
+  *out = h;
+  return RQLP_OK;
+}
+
+int rqlp_get_unique_id(void *out) {
+  if (!out) return -1;
+  try {
+    return comm_unique_id(out);
+  } catch (const std::exception &e) {
+    fprintf(stderr, "[rqlp] %s\n", e.what());
+    return RQLP_ERR_NCCL;
+  }
+}
+
+int rqlp_create_dist(rqlp_handle_t *out, int device, void *cuda_stream, const void *uid, int rank, int nranks) {
+  if (!uid) return -4;
+  if (nranks < 1) return -6;
+  if (rank < 0 || rank >= nranks) return -5;
+  int rc = rqlp_create(out, device, cuda_stream);
+  if (rc != RQLP_OK) return rc;
+  rqlp_handle_t h = *out;
+  h->rank = rank;
+  h->nranks = nranks;
+  if (nranks > 1) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    try {
+      h->comm = comm_init(uid, rank, nranks);
+    } catch (const std::exception &e) {
+      fprintf(stderr, "[rqlp] %s\n", e.what());
+      cudaSetDevice(prev);
+      rqlp_destroy(h);
+      *out = nullptr;
+      return RQLP_ERR_NCCL;
+    }
+    cudaSetDevice(prev);
+  }
+  return RQLP_OK;
+}
+
+int rqlp_destroy(rqlp_handle_t h) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  reset_timing(h);
+  if (h->own) cudaFree(h->own);
+  if (h->stage) cudaFree(h->stage);
+  if (h->dflags) cudaFree(h->dflags);
+  comm_destroy(h->comm);
+  cudaSetDevice(prev);
+  h->magic = 0;
+  delete h;
+  return RQLP_OK;
+}
+
+int rqlp_workspace_size(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
+                        size_t *bytes) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (variant < 0 || variant > 2) return -2;
+  int rc = check_common(m, n, k, p, q);
+  if (rc) return rc - 2;
+  if (variant == RQLP_VARIANT_ERQLP && d < 1) return -8;
+  int64_t l = (int64_t)k + p;
+  if (variant == RQLP_VARIANT_BRQLP && (b < 1 || b > l)) return -9;
+  if (!bytes) return -10;
+  *bytes = plan_bytes(variant, m, n, l, variant == RQLP_VARIANT_BRQLP ? b : 0, h->num_sms);
+  return RQLP_OK;
+}
+
+int rqlp_set_workspace(rqlp_handle_t h, void *ptr, size_t bytes) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (ptr && ((uintptr_t)ptr & 255)) return -2;
+  h->ws = ptr;
+  h->ws_bytes = ptr ? bytes : 0;
+  return RQLP_OK;
+}
+
+int rqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, const double *A, int64_t lda, uint64_t seed,
+            double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  int rc = check_common(m, n, k, p, q);
+  if (rc) return rc - 1;
+  int64_t l = (int64_t)k + p;
+  if (h->nranks == 1 && l > m) return -4;
+  if (!A) return -7;
+  if (lda < m) return -8;
+  if (!Q) return -10;
+  if (ldq < m) return -11;
+  if (!L) return -12;
+  if (ldl < l) return -13;
+  if (!P) return -14;
+  if (ldp < n) return -15;
+  return guarded(h, [&] {
+    return run_rqlp(h, m, n, k, p, q, 0, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
+  });
+}
+
+int erqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, const double *A, int64_t lda,
+             uint64_t seed, double *Q, int64_t ldq, double *T, int64_t ldt, int *t_is_upper, double *P, int64_t ldp,
+             int64_t *piv0) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  int rc = check_common(m, n, k, p, q);
+  if (rc) return rc - 1;
+  int64_t l = (int64_t)k + p;
+  if (h->nranks == 1 && l > m) return -4;
+  if (d < 1) return -7;
+  if (!A) return -8;
+  if (lda < m) return -9;
+  if (!Q) return -11;
+  if (ldq < m) return -12;
+  if (!T) return -13;
+  if (ldt < l) return -14;
+  if (!P) return -16;
+  if (ldp < n) return -17;
+  if (t_is_upper) *t_is_upper = (d % 2 == 0) ? 1 : 0;
+  return guarded(h, [&] {
+    return run_rqlp(h, m, n, k, p, q, d, A, lda, seed, Q, ldq, T, ldt, P, ldp, piv0, nullptr, true);
+  });
+}
+
+int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A, int64_t lda,
+             uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp, int64_t *piv0,
+             int64_t *piv1) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  int rc = check_common(m, n, k, p, q);
+  if (rc == -5) return -7;
+  if (rc) return rc - 1;
+  int64_t l = (int64_t)k + p;
+  if (h->nranks == 1 && l > m) return -4;
+  if (b < 1 || b > l) return -6;
+  if (!A) return -8;
+  if (lda < m) return -9;
+  if (!Q) return -11;
+  if (ldq < m) return -12;
+  if (!L) return -13;
+  if (ldl < l) return -14;
+  if (!P) return -15;
+  if (ldp < n) return -16;
+  return guarded(h, [&] {
+    return run_brqlp(h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
+  });
+}
+
+static bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static std::mutex g_default_mu;
+static rqlp_handle_t g_default[64] = {nullptr};
+
+int rqlp(int64_t m, int64_t n, int k, int p, int q, const double *A, int64_t lda, uint64_t seed, double *Q, double *L,
+         double *P) {
+  int rc = check_common(m, n, k, p, q);
+  if (rc) return rc;
+  int64_t l = (int64_t)k + p;
+  if (l > m) return -3;
+  if (!A) return -6;
+  if (lda < m) return -7;
+  if (!Q) return -9;
+  if (!L) return -10;
+  if (!P) return -11;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return RQLP_ERR_CUDA;
+  rqlp_handle_t h;
+  {
+    std::lock_guard<std::mutex> lk(g_default_mu);
+    if (dev >= 64) return RQLP_ERR_INTERNAL;
+    if (!g_default[dev]) {
+      int r = rqlp_create(&g_default[dev], dev, nullptr);
+      if (r) return r;
+    }
+    h = g_default[dev];
+  }
+  return guarded(h, [&] {
+    bool dA = is_device_ptr(A), dQ = is_device_ptr(Q), dL = is_device_ptr(L), dP = is_device_ptr(P);
+    // staging for host operands (the end-to-end path): A, Q, L, P device copies
+    size_t szA = dA ? 0 : (size_t)round_up(lda * n, 32) * 8;
+    size_t szQ = dQ ? 0 : (size_t)round_up(m * l, 32) * 8;
+    size_t szL = dL ? 0 : (size_t)round_up(l * l, 32) * 8;
+    size_t szP = dP ? 0 : (size_t)round_up(n * l, 32) * 8;
+    size_t tot = szA + szQ + szL + szP + 1024;
+    if (tot > 1024 && h->stage_bytes < tot) {
+      if (h->stage) cudaFree(h->stage);
+      h->stage = nullptr;
+      h->stage_bytes = 0;
+      RQLP_CUDA(cudaMalloc(&h->stage, tot));
+      h->stage_bytes = tot;
+    }
+    char *sp = (char *)h->stage;
+    const double *Ad = A;
+    double *Qd = Q, *Ld = L, *Pd = P;
+    if (!dA) { Ad = (const double *)sp; sp += szA; }
+    if (!dQ) { Qd = (double *)sp; sp += szQ; }
+    if (!dL) { Ld = (double *)sp; sp += szL; }
+    if (!dP) { Pd = (double *)sp; sp += szP; }
+    if (!dA) RQLP_CUDA(cudaMemcpyAsync((void *)Ad, A, (size_t)lda * n * 8, cudaMemcpyHostToDevice, h->stream));
+    int r = run_rqlp(h, m, n, k, p, q, 0, Ad, lda, seed, Qd, m, Ld, l, Pd, n, nullptr, nullptr, true);
+    if (r) return r;
+    if (!dQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dL) RQLP_CUDA(cudaMemcpyAsync(L, Ld, (size_t)l * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    return RQLP_OK;
+  });
+}
+
+int rqlp_sync(rqlp_handle_t h, unsigned *flags) {
+  return guarded(h, [&] {
+    RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    if (flags) {
+      unsigned f = 0;
+      RQLP_CUDA(cudaMemcpy(&f, h->dflags + FLAG_WORD, sizeof(unsigned), cudaMemcpyDeviceToHost));
+      *flags = f;
+    }
+    return RQLP_OK;
+  });
+}
+
+const char *rqlp_strerror(int code) {
+  switch (code) {
+    case RQLP_OK: return "success";
+    case RQLP_ERR_CUDA: return "CUDA runtime error";
+    case RQLP_ERR_NCCL: return "NCCL error";
+    case RQLP_ERR_WORKSPACE: return "workspace missing or too small";
+    case RQLP_ERR_INTERNAL: return "internal error";
+    case RQLP_ERR_DEVICE: return "device is not sm_100 (B200)";
+    case RQLP_ERR_HANDLE: return "invalid handle";
+    default: return code < 0 ? "illegal argument (-code = position)" : "unknown error";
+  }
+}
+
+// ---- stage entry points -------------------------------------------------------------------
+int rqlp_omega(rqlp_handle_t h, int64_t n, int64_t l, uint64_t seed, double *Om, int64_t ldo) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (n < 1) return -2;
+  if (l < 1) return -3;
+  if (!Om) return -5;
+  if (ldo < n) return -6;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    launch_omega(c, n, l, 0, seed, Om, ldo);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_gemm_nn(rqlp_handle_t h, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+                 int64_t ldx, double *Y, int64_t ldy) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 0) return -2;
+  if (cc < 0) return -3;
+  if (k < 0) return -4;
+  if (!A && m * k > 0) return -5;
+  if (lda < std::max<int64_t>(1, m)) return -6;
+  if (!X && k * cc > 0) return -7;
+  if (ldx < std::max<int64_t>(1, k)) return -8;
+  if (!Y && m * cc > 0) return -9;
+  if (ldy < std::max<int64_t>(1, m)) return -10;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    size_t pe = gemm_partials_needed(m, cc, k, c.num_sms);
+    char *ws = get_ws(h, pe * 8 + 256, true);
+    if (m > 0 && cc > 0) gemm_nn(c, m, cc, k, A, lda, X, ldx, Y, ldy, (double *)ws, pe);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_gemm_tn(rqlp_handle_t h, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
+                 int64_t ldv, double *Z, int64_t ldz, int trans_out) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 0) return -2;
+  if (cc < 0) return -3;
+  if (k < 0) return -4;
+  if (!A && m * k > 0) return -5;
+  if (lda < std::max<int64_t>(1, m)) return -6;
+  if (!V && m * cc > 0) return -7;
+  if (ldv < std::max<int64_t>(1, m)) return -8;
+  if (!Z && k * cc > 0) return -9;
+  if (ldz < std::max<int64_t>(1, trans_out ? cc : k)) return -10;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    size_t pe = gemm_partials_needed(k, cc, m, c.num_sms);
+    char *ws = get_ws(h, pe * 8 + 256, true);
+    if (k > 0 && cc > 0) {
+      if (m == 0) launch_copy(c, trans_out ? cc : k, trans_out ? k : cc, nullptr, 0, Z, ldz, false);
+      else gemm_tn(c, m, cc, k, A, lda, V, ldv, Z, ldz, trans_out != 0, (double *)ws, pe);
+    }
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_orth(rqlp_handle_t h, int64_t m, int64_t cc, const double *Y, int64_t ldy, double *V, int64_t ldv, double *R,
+              int64_t ldr) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 1) return -2;
+  if (cc < 1 || cc > m) return -3;
+  if (!Y) return -4;
+  if (ldy < m) return -5;
+  if (!V || V == Y) return -6;
+  if (ldv < m) return -7;
+  if (R && ldr < cc) return -9;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    Arena a;
+    OrthScratch s;
+    orth_carve(a, s, m, cc, c.num_sms);
+    size_t need = a.used + 256;
+    a = Arena();
+    a.base = get_ws(h, need, true);
+    a.cap = need;
+    orth_carve(a, s, m, cc, c.num_sms);
+    RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+    orth(c, s, m, cc, Y, ldy, V, ldv, R, ldr, false);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_cpqr(rqlp_handle_t h, int64_t rows, int64_t cols, const double *M, int64_t ldm, double *Q, int64_t ldq,
+              double *R, int64_t ldr, int64_t *perm) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (rows < 1 || rows > 24576) return -2;
+  if (cols < 1) return -3;
+  if (!M) return -4;
+  if (ldm < rows) return -5;
+  int64_t s = std::min(rows, cols);
+  if (Q && ldq < rows) return -7;
+  if (R && ldr < s) return -9;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    Arena a;
+    HHScratch hs;
+    int64_t ldw = round_up(rows, 8);
+    a.take<double>(ldw * cols);
+    hh_carve(a, hs, rows, cols, c.num_sms);
+    size_t need = a.used + 256;
+    a = Arena();
+    a.base = get_ws(h, need, true);
+    a.cap = need;
+    double *Wk = a.take<double>(ldw * cols);
+    hh_carve(a, hs, rows, cols, c.num_sms);
+    launch_copy(c, rows, cols, M, ldm, Wk, ldw, false);
+    hh_factor(c, hs, rows, cols, Wk, ldw, true);
+    if (R) hh_extract_r(c, hs, rows, cols, Wk, ldw, R, ldr, false);
+    if (Q) hh_form_q(c, hs, rows, cols, Q, ldq);
+    if (perm) hh_copy_perm(c, hs, cols, perm);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_qlp_tail(rqlp_handle_t h, int64_t l, int64_t n, const double *B, int64_t ldb, int d, double *QB, int64_t ldqb,
+                  double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1, int *t_is_upper) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (l < 1) return -2;
+  if (n < l) return -3;
+  if (!B) return -4;
+  if (ldb < l) return -5;
+  if (d < 0) return -6;
+  if (!QB) return -7;
+  if (ldqb < l) return -8;
+  if (!T) return -9;
+  if (ldt < l) return -10;
+  if (!PB) return -11;
+  if (ldpb < n) return -12;
+  if (t_is_upper) *t_is_upper = (d >= 2 && d % 2 == 0) ? 1 : 0;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    Arena a;
+    TailScratch s;
+    tail_carve(a, s, l, n, c.num_sms);
+    size_t need = a.used + 256;
+    a = Arena();
+    a.base = get_ws(h, need, true);
+    a.cap = need;
+    tail_carve(a, s, l, n, c.num_sms);
+    RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+    launch_copy(c, l, n, B, ldb, s.Bw, s.ldl, false);
+    qlp_tail(c, s, l, n, s.Bw, s.ldl, d, QB, ldqb, T, ldt, PB, ldpb, piv0, piv1);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_residual_sq(rqlp_handle_t h, int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, const double *Q,
+                     int64_t ldq, const double *T, int64_t ldt, const double *P, int64_t ldp, double *res_dev) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 1) return -2;
+  if (n < 1) return -3;
+  if (l < 1) return -4;
+  if (!A) return -5;
+  if (lda < m) return -6;
+  if (!Q) return -7;
+  if (ldq < m) return -8;
+  if (!T) return -9;
+  if (ldt < l) return -10;
+  if (!P) return -11;
+  if (ldp < n) return -12;
+  if (!res_dev) return -13;
+  return guarded(h, [&] {
+    Ctx c = make_ctx(h);
+    int64_t ldl = round_up(l, 8);
+    size_t need = ((size_t)ldl * n + 4096 * (size_t)n + 2048) * 8 + 1024;
+    char *ws = get_ws(h, need, true);
+    double *M = (double *)ws;  // M = T P^T  (l x n)
+    gemm_generic_ex(c, false, true, l, n, l, 1.0, T, ldt, P, ldp, 0.0, M, ldl, nullptr, 0, false, nullptr, 0);
+    double *part = M + round_up(ldl * n, 32);
+    residual_sq(c, m, n, l, A, lda, Q, ldq, M, ldl, part, res_dev);
+    h->launches = c.launches;
+    return RQLP_OK;
+  });
+}
+
+int rqlp_set_timing(rqlp_handle_t h, int enable) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  h->timing = enable != 0;
+  return RQLP_OK;
+}
+
+int rqlp_get_timing(rqlp_handle_t h, const char **names, float *ms, int capacity) {
+  if (!valid(h)) return -RQLP_ERR_HANDLE;
+  int rc = guarded(h, [&] {
+    RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    h->names_out.clear();
+    h->ms_out.clear();
+    for (size_t i = 1; i < h->events.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, h->events[i - 1].second, h->events[i].second);
+      h->names_out.push_back(h->events[i].first);
+      h->ms_out.push_back(t);
+    }
+    return RQLP_OK;
+  });
+  if (rc) return -rc;
+  int nout = (int)h->names_out.size();
+  for (int i = 0; i < nout && i < capacity; ++i) {
+    if (names) names[i] = h->names_out[i].c_str();
+    if (ms) ms[i] = h->ms_out[i];
+  }
+  return nout;
+}
+
+int64_t rqlp_launch_count(rqlp_handle_t h) { return valid(h) ? h->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// internal.cuh -- shared declarations of librqlp's sm_100a kernels and host launchers.
+// Nothing here is shared with oracle/ (the CUDA path and the oracle share no code).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rqlp.h"
+
+namespace rqlpk {
+
+// Thrown by host orchestration on a CUDA failure; converted to RQLP_ERR_CUDA at the C ABI.
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define RQLP_CUDA(call)                                                                        \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      throw ::rqlpk::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +      \
+                              __FILE__ + ":" + std::to_string(__LINE__));                      \
+  } while (0)
+
+#define RQLP_LAUNCHED(ctx)                                                                     \
+  do {                                                                                         \
+    (ctx).launches++;                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      throw ::rqlpk::CudaError(std::string("launch: ") + cudaGetErrorString(e_) + " @" +        \
+                              __FILE__ + ":" + std::to_string(__LINE__));                      \
+  } while (0)
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Device-side flag words (one per handle, in the workspace).
+enum DevFlag : int {
+  FLAG_WORD = 0,       // RQLP_FLAG_* bits accumulated by the last call
+  COND_WORD = 1,       // scratch condition for conditionally executed kernels
+  BAR_COUNT = 2,       // cooperative grid barrier (count, generation)
+  BAR_GEN = 3,
+  NUM_DEV_FLAGS = 8
+};
+
+// Execution context of one call: stream, SM count, launch counter, device flag words.
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  int64_t launches = 0;
+  unsigned *dflags = nullptr;     // NUM_DEV_FLAGS words of device memory
+  bool timing = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> *events = nullptr;
+  void mark(const char *name);
+  // row-sharded runs (comm.cu): NCCL communicator, rank, number of ranks
+  void *comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t collectives = 0;
+};
+
+// ---- NCCL (comm.cu) ----
+int comm_unique_id(void *out);
+void *comm_init(const void *uid, int rank, int nranks);
+void comm_destroy(void *comm);
+void allreduce_sum(Ctx &c, double *buf, int64_t count);
+
+// Bump allocator over a workspace; base == nullptr measures only.
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0, used = 0;
+  template <typename T>
+  T *take(int64_t count) {
+    size_t bytes = (size_t)(count > 0 ? count : 1) * sizeof(T);
+    size_t off = (used + 255) & ~(size_t)255;
+    used = off + bytes;
+    if (base && used > cap) throw std::runtime_error("workspace overflow");
+    return base ? reinterpret_cast<T *>(base + off) : nullptr;
+  }
+};
+
+// ---- Ω (omega.cu) ----
+void launch_omega(Ctx &c, int64_t n, int64_t l, int64_t col0, uint64_t seed, double *Om, int64_t ldo);
+
+// ---- GEMM (gemm.cu) ----
+// C = alpha op(A) op(B) + beta C (generic DMMA kernel; any layout / alignment).
+void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                  int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                  const unsigned *cond = nullptr, unsigned cond_mask = 0);
+// Y = A X  (A m x k, X k x c): tall-skinny pass.  Scratch for split-K partials.
+void gemm_nn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+             int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems,
+             const unsigned *cond = nullptr, unsigned cond_mask = 0);
+// Z = A^T V (k x c) or Z^T (c x k) when trans_out.
+void gemm_tn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
+             int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
+             const unsigned *cond = nullptr, unsigned cond_mask = 0);
+size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms);
+
+// ---- small dense (dense.cu) ----
+void launch_copy(Ctx &c, int64_t rows, int64_t cols, const double *S, int64_t lds, double *D, int64_t ldd,
+                 bool transpose, const unsigned *cond = nullptr, unsigned cond_mask = 0);
+void launch_fill(Ctx &c, int64_t rows, int64_t cols, double *D, int64_t ldd, double diag, double off);
+void launch_zero_u32(Ctx &c, unsigned *p, int64_t count);
+
+// ---- orthonormalisation (orth.cu) ----
+struct OrthScratch {
+  double *G = nullptr, *G2 = nullptr, *R = nullptr, *Rinv = nullptr, *Racc = nullptr, *tmp = nullptr;
+  double *Ybuf = nullptr;       // m x c ping-pong buffer
+  int64_t ldy = 0;
+  double *partials = nullptr;
+  size_t partial_elems = 0;
+  double *scal = nullptr;       // small device scalars
+};
+void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms);
+// V = orth(Y) (CholeskyQR2 + conditional shifted pass).  Y is preserved; Y and V must not alias.  R (nullable) receives the c x c triangular factor (Y = V R).
+// sharded: Y is a row block of a row-sharded matrix -> the Gram is summed over ranks.
+void orth(Ctx &ctx, OrthScratch &s, int64_t m, int64_t c, const double *Y, int64_t ldy, double *V, int64_t ldv,
+          double *R, int64_t ldr, bool sharded = false);
+
+// ---- Householder engine + QLP tail (householder.cu, tail.cu) ----
+struct HHScratch {
+  double *Vst = nullptr;        // rows x steps reflector store
+  double *tau = nullptr, *beta = nullptr, *vn1 = nullptr, *vn2 = nullptr, *slot_val = nullptr;
+  int *done = nullptr, *slot_idx = nullptr;
+  int64_t *perm = nullptr;
+  int64_t max_rows = 0, max_cols = 0, max_slots = 0;
+};
+void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms);
+// In-place Householder QR (pivot: column-pivoted, Golub + LAPACK downdating) of M.
+// Outputs in s: Vst, tau, beta, perm (full permutation).  M keeps R entries above the diagonal
+// of each step's pivot column in ORIGINAL column positions.
+void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot);
+// R (steps x cols, pivot order, sign-normalised) or its transpose (cols x steps).
+void hh_extract_r(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, const double *M, int64_t ldm, double *R,
+                  int64_t ldr, bool transpose);
+// Explicit Q (rows x steps), sign-normalised.
+void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq);
+void hh_copy_perm(Ctx &c, HHScratch &s, int64_t count, int64_t *dst);
+
+struct TailScratch {
+  double *Bw = nullptr, *Rt = nullptr, *Qhat = nullptr, *Rhat = nullptr, *Q0 = nullptr, *Qt = nullptr,
+         *Lt = nullptr, *Mt = nullptr, *QE = nullptr, *PO = nullptr, *tmp_ll = nullptr, *tmp_nl = nullptr;
+  int64_t ldn = 0, ldl = 0;
+  int64_t *perm0 = nullptr, *perm1 = nullptr;
+  HHScratch hh;
+  OrthScratch orth;
+};
+void tail_carve(Arena &a, TailScratch &s, int64_t l, int64_t n, int num_sms);
+// B (l x n) is overwritten.  Outputs QB (l x l), T, PB (n x l), piv0/piv1 (device int64, nullable).
+void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t ldb, int d, double *QB,
+              int64_t ldqb, double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1);
+
+// ---- residual (dense.cu) ----
+void residual_sq(Ctx &c, int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, const double *Q,
+                 int64_t ldq, const double *M, int64_t ldmm, double *partials, double *out);
+
+}  // namespace rqlpk

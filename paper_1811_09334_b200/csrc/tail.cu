@@ -1,0 +1,147 @@
+// tail.cu -- the small dense tail that turns B = V^T A (l x n) into B = Q_B T P_B^T.
+//
+// RQLP (d == 0), Alg.1 l.5-7:
+//   [Q0, R0, Π0] = cpqr(B);  [Q1, L^T, Π1] = cpqr(R0^T);  Q_B = Q0 Π1,  P_B = Π0 Q1.
+// ERQLP (d >= 1), Alg.2 l.5-9 with the corrected assembly (reading R9):
+//   [Q^(i), R^(i)] = qr([R^(i-1)]^T), Q_B = Q^(0) Q^(2) .., P_B = Π0 Q^(1) Q^(3) ..,
+//   T = [R^(d)]^T (lower) for odd d, R^(d) (upper) for even d.
+// B200 formulation (same result in exact arithmetic, reading R6): the
+// tall n x l R0^T is first reduced by CholeskyQR2 (BLAS-3, orth.cu) to R0^T = Q^ R^, then the
+// l x l R^ goes through the Householder engine (pivoted for RQLP: cpqr(R0^T) and cpqr(R^) pick
+// the same pivots because column norms and their downdates are orthogonally invariant).
+// The order of the n - l non-pivot columns of R0 is ascending original index; P = Π0 Q1 does
+// not depend on it.
+#include "internal.cuh"
+
+namespace rqlpk {
+
+void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                     int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc, double *partials,
+                     size_t partial_elems, bool trans_out, const unsigned *cond, unsigned cond_mask);
+
+namespace {
+
+__global__ void gather_cols_kernel(int64_t rows, int64_t cols, const double *S, int64_t lds, const int64_t *perm,
+                                   double *D, int64_t ldd) {
+  int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e % rows, t = e / rows;
+    D[i + t * ldd] = S[i + perm[t] * lds];
+  }
+}
+
+// D(perm[i], :) = S(i, :)
+__global__ void scatter_rows_kernel(int64_t rows, int64_t cols, const double *S, int64_t lds, const int64_t *perm,
+                                    double *D, int64_t ldd) {
+  int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e % rows, j = e / rows;
+    D[perm[i] + j * ldd] = S[i + j * lds];
+  }
+}
+
+__global__ void iota_kernel(int64_t count, int64_t *dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = i;
+}
+
+__global__ void copy_i64_kernel(int64_t count, const int64_t *src, int64_t *dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+int grid_for(Ctx &c, int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), (int64_t)c.num_sms * 16));
+}
+
+}  // namespace
+
+void tail_carve(Arena &a, TailScratch &s, int64_t l, int64_t n, int num_sms) {
+  s.ldn = round_up(n, 8);
+  s.ldl = round_up(l, 8);
+  s.Bw = a.take<double>(s.ldl * n);
+  s.Rt = a.take<double>(s.ldn * l);
+  s.Qhat = a.take<double>(s.ldn * l);
+  s.tmp_nl = a.take<double>(s.ldn * l);
+  s.Rhat = a.take<double>(s.ldl * l);
+  s.Q0 = a.take<double>(s.ldl * l);
+  s.Qt = a.take<double>(s.ldl * l);
+  s.Lt = a.take<double>(s.ldl * l);
+  s.Mt = a.take<double>(s.ldl * l);
+  s.QE = a.take<double>(s.ldl * l);
+  s.tmp_ll = a.take<double>(s.ldl * l);
+  s.perm0 = a.take<int64_t>(n);
+  s.perm1 = a.take<int64_t>(l);
+  hh_carve(a, s.hh, l, n, num_sms);
+  orth_carve(a, s.orth, n, l, num_sms);
+}
+
+void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t ldb, int d, double *QB, int64_t ldqb,
+              double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1) {
+  const int64_t ldn = s.ldn, ldl = s.ldl;
+  // [Q0, R0, Π0] = cpqr(B)  (Alg.1 l.5)
+  hh_factor(c, s.hh, l, n, B, ldb, true);
+  copy_i64_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, s.hh.perm, s.perm0);
+  RQLP_LAUNCHED(c);
+  hh_extract_r(c, s.hh, l, n, B, ldb, s.Rt, ldn, true);   // R0^T, n x l
+  hh_form_q(c, s.hh, l, n, s.Q0, ldl);                      // Q0, l x l
+  c.mark("tail_cpqr_B");
+  // R0^T = Q^ R^ (CholeskyQR2; the tall part of cpqr(R0^T) / the i = 1 inner QR)
+  orth(c, s.orth, n, l, s.Rt, ldn, s.Qhat, ldn, s.Rhat, ldl);
+  c.mark("tail_qr_R0T");
+  double *PO;
+  if (d == 0) {
+    // [Q~, L^T, Π1] = cpqr(R^)  (Alg.1 l.6 on the orthogonally equivalent l x l factor)
+    launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, false);
+    hh_factor(c, s.hh, l, l, s.Mt, ldl, true);
+    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.hh.perm, s.perm1);
+    RQLP_LAUNCHED(c);
+    hh_extract_r(c, s.hh, l, l, s.Mt, ldl, T, ldt, true);  // L = (L^T)^T, lower
+    hh_form_q(c, s.hh, l, l, s.Qt, ldl);
+    gemm_nn(c, n, l, l, s.Qhat, ldn, s.Qt, ldl, s.tmp_nl, ldn, s.orth.partials, s.orth.partial_elems);  // Q1
+    PO = s.tmp_nl;
+    gather_cols_kernel<<<grid_for(c, l * l), 256, 0, c.stream>>>(l, l, s.Q0, ldl, s.perm1, QB, ldqb);  // Q0 Π1
+    RQLP_LAUNCHED(c);
+    if (piv1) {
+      copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm1, piv1);
+      RQLP_LAUNCHED(c);
+    }
+  } else {
+    launch_copy(c, l, l, s.Q0, ldl, s.QE, ldl, false);
+    PO = s.Qhat;
+    double *Pspare = s.tmp_nl;
+    double *Rcur = s.Rhat;
+    for (int i = 2; i <= d; ++i) {
+      launch_copy(c, l, l, Rcur, ldl, s.Mt, ldl, true);      // [R^(i-1)]^T
+      hh_factor(c, s.hh, l, l, s.Mt, ldl, false);
+      hh_extract_r(c, s.hh, l, l, s.Mt, ldl, s.Lt, ldl, false);  // R^(i)
+      hh_form_q(c, s.hh, l, l, s.Qt, ldl);                       // Q^(i)
+      if (i % 2 == 0) {
+        gemm_generic_ex(c, false, false, l, l, l, 1.0, s.QE, ldl, s.Qt, ldl, 0.0, s.tmp_ll, ldl, s.orth.partials,
+                        s.orth.partial_elems, false, nullptr, 0);
+        launch_copy(c, l, l, s.tmp_ll, ldl, s.QE, ldl, false);
+      } else {
+        gemm_nn(c, n, l, l, PO, ldn, s.Qt, ldl, Pspare, ldn, s.orth.partials, s.orth.partial_elems);
+        std::swap(PO, Pspare);
+      }
+      launch_copy(c, l, l, s.Lt, ldl, s.Rhat, ldl, false);
+      Rcur = s.Rhat;
+    }
+    launch_copy(c, l, l, Rcur, ldl, T, ldt, d % 2 == 1);   // T = [R^(d)]^T (odd d) or R^(d) (even d)
+    launch_copy(c, l, l, s.QE, ldl, QB, ldqb, false);
+    if (piv1) {
+      iota_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, piv1);
+      RQLP_LAUNCHED(c);
+    }
+  }
+  // P_B = Π0 P1: row perm0[i] of P_B is row i of P1
+  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, PB, ldpb);
+  RQLP_LAUNCHED(c);
+  if (piv0) {
+    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm0, piv0);
+    RQLP_LAUNCHED(c);
+  }
+  c.mark("tail_assemble");
+}
+
+}  // namespace rqlpk

@@ -1,0 +1,179 @@
+"""GPU-vs-oracle parity through the C ABI (librqlp.so).  All tests need a B200 (-m gpu).
+
+Tolerances are BASELINE.json north_star's: identical pivots; L-values relative 1e-10 for
+σ_j/σ_1 >= 1e-8; residual ‖A−QLPᵀ‖_F/‖A‖_F within 1e-12 absolute; ‖QᵀQ−I‖_max <= 1e-13·l.
+Per-stage GEMM tolerances: |ΔY_ij| <= 64 u k (|A||X|)_ij.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def rq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1811_09334_b200 as rq
+    rq.lib()
+    return rq
+
+
+def _cm(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64).T)).cuda().t()
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    return np.asfortranarray(t.detach().cpu().numpy())
+
+
+def _rand_svd(m, n, sig, seed):
+    rng = np.random.default_rng(seed)
+    U_, _ = np.linalg.qr(rng.standard_normal((m, len(sig))))
+    V_, _ = np.linalg.qr(rng.standard_normal((n, len(sig))))
+    return np.asfortranarray((U_ * sig) @ V_.T)
+
+
+# ------------------------------------------------------------------ stages
+@pytest.mark.parametrize("n,l,seed", [(800, 25, 1), (4097, 110, 2), (1, 1, 0), (33, 7, 2**64 - 1), (1029, 138, 77)])
+def test_omega_bit_exact(rq, orc, n, l, seed):
+    Om = _np(rq.omega(n, l, seed))
+    ref = orc.omega(seed, n, l)
+    assert np.array_equal(Om.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("m,k,c", [(1000, 800, 25), (1031, 1030, 110), (4133, 1029, 138), (517, 93, 17), (64, 64, 64),
+                                   (3, 5, 2)])
+def test_gemm_nn_parity(rq, orc, m, k, c):
+    rng = np.random.default_rng(m + k + c)
+    A, X = rng.standard_normal((m, k)), rng.standard_normal((k, c))
+    Y = _np(rq.gemm_nn(_cm(A), _cm(X)))
+    ref = orc.gemm_nn(A, X)
+    bound = 64 * U * k * (np.abs(A) @ np.abs(X))
+    assert np.all(np.abs(Y - ref) <= bound)
+
+
+@pytest.mark.parametrize("m,k,c,trans", [(1000, 800, 25, True), (1031, 1030, 110, False), (4133, 1029, 138, True),
+                                         (517, 93, 17, False), (5, 3, 2, True)])
+def test_gemm_tn_parity(rq, orc, m, k, c, trans):
+    rng = np.random.default_rng(m * 3 + k + c)
+    A, V = rng.standard_normal((m, k)), rng.standard_normal((m, c))
+    Z = _np(rq.gemm_tn(_cm(A), _cm(V), trans_out=trans))
+    ref = orc.gemm_tn(A, V)
+    if trans:
+        ref = ref.T
+    bound = 64 * U * m * (np.abs(A).T @ np.abs(V))
+    if trans:
+        bound = bound.T
+    assert np.all(np.abs(Z - ref) <= bound)
+
+
+@pytest.mark.parametrize("m,c,cond", [(1000, 25, 1e2), (4133, 138, 1e4), (2000, 300, 1e5), (777, 129, 1e9)])
+def test_orth_matches_householder(rq, orc, m, c, cond):
+    """CholeskyQR2 (+ shifted pass when cond(Y) is large) reproduces the unique thin Q, R of
+    Householder QR with R_ii >= 0 (reading R3)."""
+    Y = _rand_svd(m, c, np.logspace(0, -np.log10(cond), c), m + c)
+    V, R = rq.orth(_cm(Y), return_r=True)
+    V, R = _np(V), _np(R)
+    Qo, Ro = orc.hqr(Y)
+    assert np.abs(V.T @ V - np.eye(c)).max() <= 1e-13 * c
+    tol = 1e-15 * cond * c
+    assert np.abs(V - Qo).max() <= max(tol, 1e-13)
+    assert np.abs(R - Ro).max() <= max(tol, 1e-13) * np.abs(Ro).max()
+
+
+@pytest.mark.parametrize("rows,cols", [(25, 800), (110, 4096), (64, 5000), (40, 40), (30, 17)])
+def test_cpqr_parity(rq, orc, rows, cols):
+    rng = np.random.default_rng(rows * cols)
+    M = rng.standard_normal((rows, cols)) * np.logspace(0, -4, cols)[rng.permutation(cols)]
+    Q, R, perm = rq.cpqr(_cm(M))
+    Qo, Ro, permo = orc.cpqr(M)
+    s = min(rows, cols)
+    perm = perm.cpu().numpy()
+    assert np.array_equal(perm[:s], permo[:s])
+    R = _np(R)
+    # columns past s: compare as a set-permuted R (non-pivot order may differ, reading R5/§8(c.1))
+    np.testing.assert_allclose(R[:, :s], Ro[:, :s], atol=1e-13 * np.abs(Ro).max())
+    np.testing.assert_allclose(_np(Q), Qo, atol=1e-12)
+
+
+@pytest.mark.parametrize("d", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("l,n", [(25, 800), (110, 1030)])
+def test_qlp_tail_parity(rq, orc, d, l, n):
+    rng = np.random.default_rng(l + n + d)
+    B = _rand_svd(l, n, np.logspace(0, -4, l), l * n)
+    g = rq.qlp_tail(_cm(B), d=d)
+    o = orc.qlp_tail(B, d=d)
+    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"])
+    assert np.array_equal(g["piv1"].cpu().numpy(), o["piv1"])
+    assert g["t_is_upper"] == o["t_is_upper"]
+    T, To = _np(g["T"]), o["T"]
+    np.testing.assert_allclose(np.diag(T), np.diag(To), rtol=1e-10)
+    np.testing.assert_allclose(T, To, atol=1e-12 * np.abs(To).max())
+    np.testing.assert_allclose(_np(g["QB"]), o["QB"], atol=1e-11)
+    np.testing.assert_allclose(_np(g["PB"]), o["PB"], atol=1e-11)
+
+
+# ------------------------------------------------------------------ end to end
+def _check_factorization(rq, orc, A, g, o, l, sig_ratio=None):
+    """north_star tolerances."""
+    An = np.linalg.norm(A)
+    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), "piv0 differ"
+    if g.get("piv1") is not None:
+        assert np.array_equal(g["piv1"].cpu().numpy(), o["piv1"]), "piv1 differ"
+    Lg, Lo = np.diag(_np(g["T"])), np.diag(o["T"])
+    mask = np.ones(l, bool) if sig_ratio is None else sig_ratio >= 1e-8
+    rel = np.abs(Lg - Lo)[mask] / np.abs(Lo)[mask]
+    assert rel.max() <= 1e-10, f"L-values rel diff {rel.max()}"
+    Qg, Pg, Tg = _np(g["Q"]), _np(g["P"]), _np(g["T"])
+    rg = orc.residual(A, Qg, Tg, Pg) / An
+    ro = orc.residual(A, o["Q"], o["T"], o["P"]) / An
+    assert abs(rg - ro) <= 1e-12, (rg, ro)
+    assert np.abs(Qg.T @ Qg - np.eye(l)).max() <= 1e-13 * l
+    return rg, ro
+
+
+CASES = [  # (name, m, n, k, p, q, d, sigma)
+    ("c1_rqlp", 1000, 800, 20, 5, 0, 0, lambda j: j**-2.0),
+    ("c1_erqlp", 1000, 800, 20, 5, 1, 2, lambda j: j**-2.0),
+    ("c2_small", 1031, 1030, 100, 10, 1, 2, lambda j: np.exp(-j / 50.0)),
+    ("c3_small", 2053, 1029, 122, 16, 2, 2, lambda j: 1.0 / j),
+    ("odd_d", 700, 500, 40, 8, 1, 3, lambda j: j**-1.5),
+    ("d1", 700, 500, 40, 8, 0, 1, lambda j: j**-1.5),
+    ("d4", 700, 500, 40, 8, 0, 4, lambda j: j**-1.5),
+    ("wide", 300, 900, 40, 8, 1, 0, lambda j: j**-1.0),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_end_to_end_parity(rq, orc, case):
+    name, m, n, k, p, q, d, sf = case
+    r = min(m, n)
+    sig = sf(np.arange(1, r + 1.0))
+    A = _rand_svd(m, n, sig, m + n)
+    l = k + p
+    g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=7)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=7)
+    if d >= 1:
+        o["piv1"] = None
+    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0])
+
+
+@pytest.mark.parametrize("b,q", [(64, 1), (7, 0), (16, 1), (136, 0)])
+def test_brqlp_parity(rq, orc, b, q):
+    m, n, k, p = 1500, 700, 120, 16
+    sig = np.exp(-np.arange(1, 701.0) / 100)
+    A = _rand_svd(m, n, sig, 99)
+    g = rq.factorize(_cm(A), k, p, q=q, b=b, seed=4)
+    o = orc.brqlp(A, k, p, b=b, q=q, seed=4)
+    _check_factorization(rq, orc, A, g, o, k + p)
+
+
+def test_residual_kernel(rq, orc):
+    A = _rand_svd(900, 400, np.arange(1, 401.0) ** -1, 5)
+    o = orc.rqlp(A, 30, 6, q=0, d=0, seed=1)
+    r = rq.residual(_cm(A), _cm(o["Q"]), _cm(o["T"]), _cm(o["P"]))
+    assert r == pytest.approx(orc.residual(A, o["Q"], o["T"], o["P"]), rel=1e-10)
