@@ -321,3 +321,25 @@ def residual(A, Q, T, P, handle=None) -> float:
     _check(lib().rqlp_residual_sq(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(T), _ld(T), _ptr(P), _ld(P),
                                   _ptr(out)), "rqlp_residual_sq")
     return float(out.item()) ** 0.5
+
+
+def factorize_host(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 0, b: int | None = None, seed: int = 0,
+                   handle: Handle | None = None, out: tuple | None = None):
+    """rqlp_factorize() with HOST operands (a column-major float64 CPU tensor A, ideally pinned):
+    the C call copies A to the device, factorises, copies Q, T, P back and returns.  `out` may
+    pass preallocated (pinned) column-major CPU tensors (Q, T, P)."""
+    if A.is_cuda or A.dtype != torch.float64:
+        raise TypeError("A must be a float64 CPU tensor")
+    h = _handle(handle)
+    m, n = A.shape
+    l = k + p
+    variant = VARIANT_BRQLP if b is not None else (VARIANT_ERQLP if d >= 1 else VARIANT_RQLP)
+    if out is None:
+        pin = A.is_pinned()
+        out = tuple(torch.empty(c, r, dtype=torch.float64, pin_memory=pin).t() for r, c in ((m, l), (l, l), (n, l)))
+    Q, T, P = out
+    tu = ctypes.c_int(0)
+    h.clear_workspace()
+    _check(lib().rqlp_factorize(h.h, variant, m, n, k, p, q, d, b or 0, _ptr(A), _ld(A), seed, _ptr(Q), _ptr(T),
+                                _ptr(P), ctypes.byref(tu)), "rqlp_factorize")
+    return Q, T, P, bool(tu.value)

@@ -490,6 +490,68 @@ static bool is_device_ptr(const void *p) {
 static std::mutex g_default_mu;
 static rqlp_handle_t g_default[64] = {nullptr};
 
+// Synchronous any-pointer factorisation: host operands are staged through device memory.
+static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
+                         const double *A, int64_t lda, uint64_t seed, double *Q, double *T, double *P,
+                         int *t_is_upper) {
+  int64_t l = (int64_t)k + p;
+  return guarded(h, [&] {
+    bool dA = is_device_ptr(A), dQ = is_device_ptr(Q), dT = is_device_ptr(T), dP = is_device_ptr(P);
+    size_t nA = (size_t)(lda * (n - 1) + m);
+    size_t szA = dA ? 0 : (size_t)round_up((int64_t)nA, 32) * 8;
+    size_t szQ = dQ ? 0 : (size_t)round_up(m * l, 32) * 8;
+    size_t szT = dT ? 0 : (size_t)round_up(l * l, 32) * 8;
+    size_t szP = dP ? 0 : (size_t)round_up(n * l, 32) * 8;
+    size_t tot = szA + szQ + szT + szP + 1024;
+    if (tot > 1024 && h->stage_bytes < tot) {
+      if (h->stage) cudaFree(h->stage);
+      h->stage = nullptr;
+      h->stage_bytes = 0;
+      RQLP_CUDA(cudaMalloc(&h->stage, tot));
+      h->stage_bytes = tot;
+    }
+    char *sp = (char *)h->stage;
+    const double *Ad = A;
+    double *Qd = Q, *Td = T, *Pd = P;
+    if (!dA) { Ad = (const double *)sp; sp += szA; }
+    if (!dQ) { Qd = (double *)sp; sp += szQ; }
+    if (!dT) { Td = (double *)sp; sp += szT; }
+    if (!dP) { Pd = (double *)sp; sp += szP; }
+    if (!dA) RQLP_CUDA(cudaMemcpyAsync((void *)Ad, A, nA * 8, cudaMemcpyHostToDevice, h->stream));
+    int r;
+    if (variant == RQLP_VARIANT_BRQLP)
+      r = run_brqlp(h, m, n, k, p, b, q, Ad, lda, seed, Qd, m, Td, l, Pd, n, nullptr, nullptr, true);
+    else
+      r = run_rqlp(h, m, n, k, p, q, variant == RQLP_VARIANT_ERQLP ? d : 0, Ad, lda, seed, Qd, m, Td, l, Pd, n,
+                   nullptr, nullptr, true);
+    if (r) return r;
+    if (t_is_upper) *t_is_upper = (variant == RQLP_VARIANT_ERQLP && d % 2 == 0) ? 1 : 0;
+    if (!dQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dT) RQLP_CUDA(cudaMemcpyAsync(T, Td, (size_t)l * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    return RQLP_OK;
+  });
+}
+
+int rqlp_factorize(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
+                   const double *A, int64_t lda, uint64_t seed, double *Q, double *T, double *P, int *t_is_upper) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (variant < 0 || variant > 2) return -2;
+  int rc = check_common(m, n, k, p, q);
+  if (rc) return rc - 2;
+  int64_t l = (int64_t)k + p;
+  if (h->nranks == 1 && l > m) return -5;
+  if (variant == RQLP_VARIANT_ERQLP && d < 1) return -8;
+  if (variant == RQLP_VARIANT_BRQLP && (b < 1 || b > l)) return -9;
+  if (!A) return -10;
+  if (lda < m) return -11;
+  if (!Q) return -13;
+  if (!T) return -14;
+  if (!P) return -15;
+  return factorize_any(h, variant, m, n, k, p, q, d, b, A, lda, seed, Q, T, P, t_is_upper);
+}
+
 int rqlp(int64_t m, int64_t n, int k, int p, int q, const double *A, int64_t lda, uint64_t seed, double *Q, double *L,
          double *P) {
   int rc = check_common(m, n, k, p, q);
@@ -513,37 +575,7 @@ int rqlp(int64_t m, int64_t n, int k, int p, int q, const double *A, int64_t lda
     }
     h = g_default[dev];
   }
-  return guarded(h, [&] {
-    bool dA = is_device_ptr(A), dQ = is_device_ptr(Q), dL = is_device_ptr(L), dP = is_device_ptr(P);
-    // staging for host operands (the end-to-end path): A, Q, L, P device copies
-    size_t szA = dA ? 0 : (size_t)round_up(lda * n, 32) * 8;
-    size_t szQ = dQ ? 0 : (size_t)round_up(m * l, 32) * 8;
-    size_t szL = dL ? 0 : (size_t)round_up(l * l, 32) * 8;
-    size_t szP = dP ? 0 : (size_t)round_up(n * l, 32) * 8;
-    size_t tot = szA + szQ + szL + szP + 1024;
-    if (tot > 1024 && h->stage_bytes < tot) {
-      if (h->stage) cudaFree(h->stage);
-      h->stage = nullptr;
-      h->stage_bytes = 0;
-      RQLP_CUDA(cudaMalloc(&h->stage, tot));
-      h->stage_bytes = tot;
-    }
-    char *sp = (char *)h->stage;
-    const double *Ad = A;
-    double *Qd = Q, *Ld = L, *Pd = P;
-    if (!dA) { Ad = (const double *)sp; sp += szA; }
-    if (!dQ) { Qd = (double *)sp; sp += szQ; }
-    if (!dL) { Ld = (double *)sp; sp += szL; }
-    if (!dP) { Pd = (double *)sp; sp += szP; }
-    if (!dA) RQLP_CUDA(cudaMemcpyAsync((void *)Ad, A, (size_t)lda * n * 8, cudaMemcpyHostToDevice, h->stream));
-    int r = run_rqlp(h, m, n, k, p, q, 0, Ad, lda, seed, Qd, m, Ld, l, Pd, n, nullptr, nullptr, true);
-    if (r) return r;
-    if (!dQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (!dL) RQLP_CUDA(cudaMemcpyAsync(L, Ld, (size_t)l * l * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (!dP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
-    RQLP_CUDA(cudaStreamSynchronize(h->stream));
-    return RQLP_OK;
-  });
+  return factorize_any(h, RQLP_VARIANT_RQLP, m, n, k, p, q, 0, 0, A, lda, seed, Q, L, P, nullptr);
 }
 
 int rqlp_sync(rqlp_handle_t h, unsigned *flags) {
