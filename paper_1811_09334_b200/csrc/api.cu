@@ -47,6 +47,8 @@ void Ctx::mark(const char *name) {
 
 namespace {
 
+unsigned long long *g_trace = nullptr;  // debug (RQLP_ENGINE_TRACE): engine phase timestamps
+
 bool valid(rqlp_handle_t h) { return h && h->magic == 0x51504c52; }
 
 Ctx make_ctx(rqlp_handle_t h) {
@@ -60,6 +62,10 @@ Ctx make_ctx(rqlp_handle_t h) {
   c.comm = h->comm;
   c.rank = h->rank;
   c.nranks = h->nranks;
+  if (getenv("RQLP_ENGINE_TRACE")) {
+    if (!g_trace) cudaMalloc(&g_trace, 4 * 4096 * sizeof(unsigned long long));
+    c.trace = g_trace;
+  }
   return c;
 }
 
@@ -817,5 +823,12 @@ int rqlp_get_timing(rqlp_handle_t h, const char **names, float *ms, int capacity
 }
 
 int64_t rqlp_launch_count(rqlp_handle_t h) { return valid(h) ? h->launches : -1; }
+
+// Debug only (not in rqlp.h): copy the engine phase trace (RQLP_ENGINE_TRACE=1) to the host.
+int rqlp_debug_trace(unsigned long long *host, int count) {
+  if (!g_trace || !host) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, g_trace, sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
 
 }  // extern "C"

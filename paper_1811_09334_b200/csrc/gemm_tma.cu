@@ -1,17 +1,352 @@
-// gemm_tma.cu -- TMA-pipelined DMMA kernels for the two tall-skinny A-passes (placeholder:
-// returns false so gemm.cu falls back to the generic DMMA kernel).
+// gemm_tma.cu -- TMA-pipelined FP64 DMMA kernels for the tall-skinny A-passes.
+//
+//   NN: Y (m x c) = A (m x k) X (k x c)      -- the sketch Y = AΩ (Alg.1 l.2), the
+//                                              power step Y = AW, Q = V Q_B and Y R^-1
+//   TN: Z (k x c) = A^T (k x m) V (m x c)    -- the projection B = V^T A (Alg.1 l.4, PAPER.md:98,
+//                                              written transposed), the power step A^T V, Grams
+//
+// B200 design: no FP64 tcgen05 exists, so the MMA is mma.sync m8n8k4.f64
+// (SASS DMMA.8x8x4, measured 37.07 TFLOP/s chip-wide vs 34.1 for DFMA).  A CTA owns a
+// 128 x BN output tile (BN = 16..144 chosen per c to minimise padding); 8 consumer warps
+// (4 x 2) each hold a 32 x BN/2 accumulator block in registers; thread 0 also streams
+// BK = 24-deep slabs of A and of X/V into a 4-stage shared-memory ring with TMA
+// (cp.async.bulk.tensor, mbarrier complete_tx).  The shared layouts are chosen so every
+// fragment load is bank-conflict free WITHOUT swizzling:
+//   * K-major tiles (X, V, and A in TN) are [rows][24]: 24 = 8 mod 16 doubles, so the 16-byte
+//     fragment loads (two k's per thread, feeding two DMMAs) of a quarter warp hit 32 banks.
+//   * the M-major A tile of NN is [24][130]: the TMA box is 130 rows tall (2 rows of overlap
+//     with the next tile, zero-filled past m), giving LD = 130 = 2 mod 8.
+// Split-K (gridDim.z) writes FP64 partial tiles reduced in a fixed order (deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "internal.cuh"
 
 namespace rqlpk {
 
-bool gemm_nn_tma(Ctx &, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *, int64_t,
-                 double *, size_t, const unsigned *, unsigned) {
-  return false;
+void launch_reduce(Ctx &c, int64_t M, int64_t N, int S, const double *part, double alpha, double beta, double *C,
+                   int64_t ldc, bool trans, const unsigned *cond, unsigned cond_mask);
+
+namespace {
+
+constexpr int BM = 128, BK = 24, STAGES = 4, NCONS = 8;
+constexpr int LDA_NN = BM + 2;  // doubles
+constexpr int A_TILE_BYTES_NN = ((BK * LDA_NN * 8 + 127) / 128) * 128;
+constexpr int A_TILE_BYTES_TN = BM * BK * 8;
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
-bool gemm_tn_tma(Ctx &, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *, int64_t,
-                 bool, double *, size_t, const unsigned *, unsigned) {
-  return false;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-size_t gemm_tma_partials_needed(int64_t, int64_t, int64_t, int) { return 0; }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// MODE 0 = NN, 1 = TN.  Output element (i, j) of the (M x N) product goes to
+//   part (split-K slice, M x N contiguous)  or  C[i + j ldc]  or (trans) C[j + i ldc].
+template <int BN, int MODE>
+__global__ void __launch_bounds__(NCONS * 32, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
+                    int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
+                    double *__restrict__ part, const unsigned *cond, unsigned cond_mask) {
+  if (cond && ((*cond) & cond_mask) == 0) return;
+  constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
+  constexpr int B_BYTES = BN * BK * 8;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr int NB = BN / 16;  // 8-col fragments per warp (warp tile 32 x BN/2)
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int kt0 = blockIdx.z * ktiles_per_split;
+  const int kt1 = min(ktiles_total, kt0 + ktiles_per_split);
+  const int nkt = kt1 - kt0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---------------- producer role (thread 0 of warp 0): TMA slabs STAGES-1 iterations ahead
+  auto issue = [&](int it) {
+    const int s = it % STAGES;
+    unsigned char *sa = smem + s * STAGE_BYTES;
+    unsigned char *sb = sa + A_BYTES;
+    const int kk = (kt0 + it) * BK;
+    mbar_expect_tx(&full[s], (MODE == 0 ? BK * LDA_NN * 8 : A_TILE_BYTES_TN) + B_BYTES);
+    if (MODE == 0) tma_load_2d(sa, &mapA, m0, kk, &full[s]);   // A box {BM+2, BK} at (m0, k)
+    else tma_load_2d(sa, &mapA, kk, m0, &full[s]);             // A box {BK, BM} at (k = row offset, col)
+    tma_load_2d(sb, &mapB, kk, n0, &full[s]);                  // B box {BK, BN} at (k, n0)
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapB) : "memory");
+    for (int it = 0; it < STAGES - 1 && it < nkt; ++it) issue(it);
+  }
+
+  // ---------------- consumers: 8 warps, 4 (M) x 2 (N), warp tile 32 x BN/2
+  const int wm = warp & 3, wn = warp >> 2;
+  const int r = lane >> 2, cq = lane & 3;
+  double acc[4][NB][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int it = 0; it < nkt; ++it) {
+    const int s = it % STAGES;
+    if (threadIdx.x == 0 && it + STAGES - 1 < nkt) {
+      // refill the slot consumed at iteration it-1 once every warp has released it
+      if (it >= 1) mbar_wait(&empty[(it - 1) % STAGES], ((it - 1) / STAGES) & 1);
+      issue(it + STAGES - 1);
+    }
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const double *sa = reinterpret_cast<const double *>(smem + s * STAGE_BYTES);
+    const double *sb = reinterpret_cast<const double *>(smem + s * STAGE_BYTES + A_BYTES);
+#pragma unroll
+    for (int kk = 0; kk < BK / 8; ++kk) {
+      double a0[4], a1[4];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const int row = wm * 32 + mb * 8 + r;
+        if (MODE == 0) {
+          a0[mb] = sa[(kk * 8 + 2 * cq) * LDA_NN + row];
+          a1[mb] = sa[(kk * 8 + 2 * cq + 1) * LDA_NN + row];
+        } else {
+          const double2 v = *reinterpret_cast<const double2 *>(sa + row * BK + kk * 8 + 2 * cq);
+          a0[mb] = v.x;
+          a1[mb] = v.y;
+        }
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int col = wn * (BN / 2) + nb * 8 + r;
+        const double2 b = *reinterpret_cast<const double2 *>(sb + col * BK + kk * 8 + 2 * cq);
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) {
+          dmma(acc[mb][nb][0], acc[mb][nb][1], a0[mb], b.x);
+          dmma(acc[mb][nb][0], acc[mb][nb][1], a1[mb], b.y);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue: fragment (mb, nb) holds out[row][col], out[row][col+1]
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) {
+    const int i = m0 + wm * 32 + mb * 8 + r;
+    if (i >= M) continue;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int j = n0 + wn * (BN / 2) + nb * 8 + 2 * cq;
+      if (part) {
+        double *dst = part + (size_t)blockIdx.z * M * N;
+        if (j < N) dst[i + (size_t)j * M] = acc[mb][nb][0];
+        if (j + 1 < N) dst[i + (size_t)(j + 1) * M] = acc[mb][nb][1];
+      } else if (trans) {
+        double *dst = C + j + (size_t)i * ldc;
+        if (j + 1 < N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          *reinterpret_cast<double2 *>(dst) = make_double2(acc[mb][nb][0], acc[mb][nb][1]);
+        } else {
+          if (j < N) dst[0] = acc[mb][nb][0];
+          if (j + 1 < N) dst[1] = acc[mb][nb][1];
+        }
+      } else {
+        if (j < N) C[i + (size_t)j * ldc] = acc[mb][nb][0];
+        if (j + 1 < N) C[i + (size_t)(j + 1) * ldc] = acc[mb][nb][1];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw CudaError("cuTensorMapEncodeTiled entry point unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D FP64 tensor map over a column-major (rows x cols, ld) matrix with the given box.
+bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, int64_t ld, int box0, int box1) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1) || rows <= 0 || cols <= 0) return false;
+  if (rows >= (1ll << 31) || cols >= (1ll << 31) || (uint64_t)ld * 8 >= (1ull << 40)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box,
+                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+const int kBNs[] = {16, 32, 48, 64, 80, 96, 112, 128, 144};
+
+int choose_bn(int64_t c) {
+  if (c <= 16) return 16;
+  int best = 144;
+  int64_t best_pad = INT64_MAX;
+  for (int bn : kBNs) {
+    if (bn < 64 && c > 64) continue;  // keep A re-reads bounded for wide outputs
+    int64_t pad = ceil_div(c, bn) * bn;
+    if (pad < best_pad || (pad == best_pad && bn > best)) {
+      best_pad = pad;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+// Split-K: minimise waves(T) * ceil(ktiles / S) with T = tiles * S CTAs (1 CTA per SM).
+int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems) {
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= 64; ++s) {
+    if (s > 1 && (size_t)s * out_elems > partial_cap_elems) break;
+    if (s > 1 && ktiles / s < 4) break;
+    int64_t T = tiles * s;
+    double waves = (double)ceil_div(T, num_sms);
+    double cost = waves * (double)ceil_div(ktiles, s) + (s > 1 ? 0.02 * ktiles + 2.0 : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+template <int BN, int MODE>
+void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask) {
+  constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
+  constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
+  static bool attr = false;
+  if (!attr) {
+    RQLP_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr = true;
+  }
+  int kps = (int)ceil_div(ktiles, S);
+  S = (int)ceil_div(ktiles, kps);
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
+  gemm_tma_kernel<BN, MODE><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
+                                                                       trans ? 1 : 0, S > 1 ? part : nullptr, cond,
+                                                                       mask);
+  RQLP_LAUNCHED(c);
+  if (S > 1) launch_reduce(c, M, N, S, part, 1.0, 0.0, C, ldc, trans, cond, mask);
+}
+
+template <int MODE>
+void dispatch(Ctx &c, int bn, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask) {
+  switch (bn) {
+    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+  }
+}
+
+bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RQLP_DISABLE_TMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+}  // namespace
+
+size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
+  // upper bound over both modes for the shapes (m, cc, k) and (k, cc, m)
+  size_t best = 0;
+  for (int mode = 0; mode < 2; ++mode) {
+    int64_t M = mode == 0 ? m : k, K = mode == 0 ? k : m;
+    int bn = choose_bn(cc);
+    int64_t tiles = ceil_div(M, BM) * ceil_div(cc, bn);
+    int S = choose_splits(tiles, ceil_div(K, BK), num_sms, (size_t)1 << 62, M * cc);
+    if (S > 1) best = std::max(best, (size_t)S * M * cc);
+  }
+  return best;
+}
+
+bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X, int64_t ldx,
+                 double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
+                 unsigned cond_mask) {
+  if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
+  int bn = choose_bn(cc);
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, m, k, lda, LDA_NN, BK)) return false;
+  if (!make_map(&mb, X, k, cc, ldx, BK, bn)) return false;
+  int64_t ktiles = ceil_div(k, BK);
+  int64_t tiles = ceil_div(m, BM) * ceil_div(cc, bn);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc);
+  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask);
+  return true;
+}
+
+bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
+                 double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
+                 unsigned cond_mask) {
+  if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
+  int bn = choose_bn(cc);
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, m, k, lda, BK, BM)) return false;
+  if (!make_map(&mb, V, m, cc, ldv, BK, bn)) return false;
+  int64_t ktiles = ceil_div(m, BK);
+  int64_t tiles = ceil_div(k, BM) * ceil_div(cc, bn);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc);
+  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask);
+  return true;
+}
 
 }  // namespace rqlpk

@@ -6,14 +6,18 @@
 // index; norms are downdated with the LAPACK xLAQP2 rule and recomputed when
 // t (vn1/vn2)^2 <= sqrt(2^-53).  The paper names no pivot rule; SURVEY §8(c.1) step 6 fixes it.
 //
-// B200 design: one persistent cooperative kernel runs all s = min(rows, cols) strictly
-// sequential steps.  Columns stay where they are (no physical swaps): column i is owned by
-// warp (i mod W) of the grid, which keeps its norms and applies every reflector to it; a step
-// costs one software grid barrier.  Every CTA recomputes the step's reflector from the pivot
-// column with the same fixed-order reduction, so all CTAs hold bit-identical v, τ without a
-// second barrier; one CTA stores the reflector.  The matrix lives in global memory (L2-resident
-// for the tail's sizes: B is l x n <= 1056 x 16384).  Small matrices run the same code as a
-// single 1024-thread CTA whose "grid barrier" is __syncthreads.
+// B200 design: one persistent kernel runs all s = min(rows, cols) strictly sequential steps.
+// Columns stay where they are (no physical swaps): CTA b owns columns b, b+G, b+2G, ... and
+// keeps them (and their norms) in shared memory when they fit; it applies every reflector to
+// them.  Small matrices run in ONE 1024-thread CTA entirely in shared memory (no global
+// exchange).  Larger ones run on one CTA per SM (cooperative launch); each step then needs one
+// exchange, done NCCL-LL style: every CTA publishes its best candidate (norm, column) as three
+// 8-byte words each carrying the step tag, after the candidate column's rows j.. (release
+// fence); every CTA polls all tags (the poll IS the grid barrier), takes the exact argmax
+// (ties -> lowest column) and reads the winner's column.  Records and candidate columns are
+// double-buffered by step parity, so a CTA can run at most one step ahead without overwriting
+// data a slower CTA still reads.  Every CTA recomputes the reflector from the winner's column
+// with the same fixed-order reduction, so all hold bit-identical v, tau; CTA 0 stores it.
 #include "internal.cuh"
 
 namespace rqlpk {
@@ -43,35 +47,16 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
-__device__ void grid_sync(unsigned *count, volatile unsigned *gen) {
-  __syncthreads();
-  if (gridDim.x == 1) return;
-  if (threadIdx.x == 0) {
-    unsigned g = *gen;
-    __threadfence();
-    unsigned arrived = atomicAdd(count, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd((unsigned *)gen, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Block-wide sum in a fixed order (identical in every CTA for identical inputs).
+// Block-wide sum in a fixed order (identical in every CTA for identical inputs): warp sums,
+// then warp 0 combines the per-warp sums with the same shuffle tree.
 __device__ double block_sum(double s, double *red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   s = warp_sum(s);
   __syncthreads();
   if (lane == 0) red[warp] = s;
   __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < nw; ++w) t += red[w];
-  return t;
+  double t = lane < nw ? red[lane] : 0.0;
+  return warp_sum(t);
 }
 
 __device__ double warp_norm(const double *x, int64_t len) {
@@ -84,81 +69,157 @@ struct EngineArgs {
   double *M;
   int64_t ldm;
   int rows, cols, steps, pivot;
-  double *Vst;  // rows x steps, ld rows
-  double *tau, *beta, *vn1, *vn2, *slot_val;
-  int *done, *slot_idx;
+  int owned_max;   // max columns owned by one CTA
+  double *Vst;     // rows x steps, ld rows
+  double *tau, *beta;
+  unsigned long long *rec;   // [2][G][4] LL words: {hi(val)|tag, lo(val)|tag, idx|tag, -}
+  unsigned long long *cand;  // [2][G][rows][2] LL words of the candidate column rows j.. (lo, hi halves)
+  unsigned epoch;            // high 16 bits of every tag (launch-unique, so stale words never match)
+  unsigned long long *trace; // optional per-step phase timestamps (CTA 0, thread 0), debugging only
+  int *done;                // done[col] = 1 once pivoted (compaction of the non-pivot columns)
   int64_t *perm;
-  unsigned *bar;  // [count, gen]
 };
 
+__device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
+  return ((unsigned long long)hi << 32) | tag;
+}
+
+// Shared-memory layout: vraw[rows] | vn1[owned] | vn2[owned] | colbuf[owned*rows] (SMEMC) | done_l[owned]
+//
+// Per step: (GRID only) warp 0 polls the tagged records (the exchange is the grid barrier), all
+// threads fetch the winner's rows j.. into vraw, one __syncthreads; then EVERY warp recomputes
+// the reflector from the pivot column with the same lane assignment and shuffle tree (so all
+// warps and CTAs hold identical bits, no block reduction), applies it to its own columns and
+// downdates their norms; warps post their best candidate in a parity-double-buffered slot and
+// meet at the step's single __syncthreads; every warp then reduces the 32 slots itself.
+template <bool GRID, bool SMEMC>
 __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
   extern __shared__ double smem[];
-  double *v = smem;                 // rows
-  double *red = smem + a.rows;      // 32
-  __shared__ double s_bv[32];
-  __shared__ int s_bi[32];
+  double *vraw = smem;
+  double *vn1 = vraw + a.rows;
+  double *vn2 = vn1 + a.owned_max;
+  double *colbuf = vn2 + a.owned_max;
+  int *done_l = reinterpret_cast<int *>(colbuf + (SMEMC ? (int64_t)a.owned_max * a.rows : 0));
+  __shared__ double s_bv[2][32];
+  __shared__ int s_bi[2][32];
   __shared__ int s_p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  const int W = gridDim.x * wpb, gw = blockIdx.x * wpb + warp;
-  unsigned *bcount = a.bar;
-  volatile unsigned *bgen = a.bar + 1;
-
-  // ---- init: column norms (pivoting) and candidate slots
-  Best best{-1.0, 0x7fffffff};
-  for (int i = gw; i < a.cols; i += W) {
-    if (lane == 0) a.done[i] = 0;
-    if (a.pivot) {
-      double nrm = warp_norm(a.M + (int64_t)i * a.ldm, a.rows);
-      if (lane == 0) { a.vn1[i] = nrm; a.vn2[i] = nrm; }
-      if (better(nrm, i, best.v, best.i)) { best.v = nrm; best.i = i; }
+  const int G = GRID ? (int)gridDim.x : 1, b = GRID ? (int)blockIdx.x : 0;
+  const int nown = b < a.cols ? (a.cols - b + G - 1) / G : 0;  // columns b, b+G, b+2G, ...
+  const int rows = a.rows;
+  auto colptr = [&](int li) -> double * {
+    if (SMEMC) return colbuf + (int64_t)li * rows;
+    return a.M + (int64_t)(b + li * G) * a.ldm;
+  };
+  auto cta_best = [&](int par) -> Best {  // every warp: argmax of the 32 warp slots
+    Best c = lane < wpb ? Best{s_bv[par][lane], s_bi[par][lane]} : Best{-1.0, 0x7fffffff};
+    return warp_best(c);
+  };
+  // GRID: publish this CTA's candidate for step jn (warp 0 only): candidate rows jn.. as LL words,
+  // then the tagged record {value, column}.
+  auto publish = [&](int jn, Best c) {
+    const int par = jn & 1;
+    const unsigned tag = (a.epoch << 16) | ((unsigned)jn + 1u);
+    int src = -1;
+    if (a.pivot) src = c.i != 0x7fffffff ? c.i : -1;
+    else if (jn < a.cols && jn % G == b) src = jn;
+    if (src >= 0) {
+      const double *sp = colptr((src - b) / G);
+      volatile unsigned long long *dst = a.cand + ((int64_t)par * G + b) * rows * 2;
+      for (int r = jn + lane; r < rows; r += 32) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(sp[r]);
+        dst[2 * (r - jn)] = pack((unsigned)bits, tag);
+        dst[2 * (r - jn) + 1] = pack((unsigned)(bits >> 32), tag);
+      }
     }
-  }
-  auto publish = [&]() {
-    if (!a.pivot) return;
-    Best b = warp_best(best);
-    if (lane == 0) { s_bv[warp] = b.v; s_bi[warp] = b.i; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Best c{-1.0, 0x7fffffff};
-      for (int w = 0; w < wpb; ++w)
-        if (better(s_bv[w], s_bi[w], c.v, c.i)) { c.v = s_bv[w]; c.i = s_bi[w]; }
-      a.slot_val[blockIdx.x] = c.v;
-      a.slot_idx[blockIdx.x] = c.i;
+    if (lane == 0 && (a.pivot || src >= 0)) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(a.pivot ? c.v : 0.0);
+      volatile unsigned long long *rc = a.rec + ((int64_t)par * G + b) * 4;
+      rc[0] = pack((unsigned)(bits >> 32), tag);
+      rc[1] = pack((unsigned)bits, tag);
+      rc[2] = pack((unsigned)(a.pivot ? c.i : src), tag);
     }
   };
-  publish();
-  grid_sync(bcount, bgen);
+
+  if (SMEMC)
+    for (int li = 0; li < nown; ++li)
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) colbuf[(int64_t)li * rows + r] = a.M[(int64_t)(b + li * G) * a.ldm + r];
+  for (int li = threadIdx.x; li < nown; li += blockDim.x) {
+    done_l[li] = 0;
+    a.done[b + li * G] = 0;
+  }
+  __syncthreads();
+  Best best{-1.0, 0x7fffffff};
+  if (a.pivot)
+    for (int li = warp; li < nown; li += wpb) {
+      double nrm = warp_norm(colptr(li), rows);
+      if (lane == 0) { vn1[li] = nrm; vn2[li] = nrm; }
+      if (better(nrm, b + li * G, best.v, best.i)) { best.v = nrm; best.i = b + li * G; }
+    }
+  {
+    Best wb = warp_best(best);
+    if (lane == 0) { s_bv[0][warp] = wb.v; s_bi[0][warp] = wb.i; }
+  }
+  __syncthreads();
+  if (GRID && warp == 0) publish(0, cta_best(0));
 
   for (int j = 0; j < a.steps; ++j) {
-    // ---- 1. pivot: global argmax over the CTA slots (exact, order independent)
-    if (warp == 0) {
-      int p = j;
-      if (a.pivot) {
-        Best c{-1.0, 0x7fffffff};
-        for (int s = lane; s < (int)gridDim.x; s += 32) {
-          double sv = __ldcg(a.slot_val + s);
-          int si = __ldcg(a.slot_idx + s);
-          if (better(sv, si, c.v, c.i)) { c.v = sv; c.i = si; }
-        }
-        c = warp_best(c);
-        p = c.i;
+    const int par = j & 1;
+    auto stamp = [&](int ph) {
+      if (a.trace && b == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[(int64_t)j * 4 + ph] = t;
       }
-      if (lane == 0) s_p = p;
+    };
+    stamp(0);
+    const int len = rows - j;
+    const double *cp;  // rows j.. of the pivot column
+    int p;
+    if (GRID) {
+      const unsigned tag = (a.epoch << 16) | ((unsigned)j + 1u);
+      if (warp == 0) {
+        Best c{-1.0, 0x7fffffff};
+        if (a.pivot) {
+          for (int s = lane; s < G; s += 32) {
+            volatile unsigned long long *rc = a.rec + ((int64_t)par * G + s) * 4;
+            unsigned long long w0, w1, w2;
+            do {
+              w0 = rc[0]; w1 = rc[1]; w2 = rc[2];
+            } while ((unsigned)w0 != tag || (unsigned)w1 != tag || (unsigned)w2 != tag);
+            const double val = __longlong_as_double((long long)(((w0 >> 32) << 32) | (w1 >> 32)));
+            const int idx = (int)(w2 >> 32);
+            if (better(val, idx, c.v, c.i)) { c.v = val; c.i = idx; }
+          }
+          c = warp_best(c);
+        } else {
+          c.i = j;
+        }
+        if (lane == 0) s_p = c.i;
+      }
+      __syncthreads();
+      p = s_p;
+      volatile const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * rows * 2;
+      for (int r = threadIdx.x; r < len; r += blockDim.x) {
+        unsigned long long lo, hi;
+        do { lo = src[2 * r]; } while ((unsigned)lo != tag);
+        do { hi = src[2 * r + 1]; } while ((unsigned)hi != tag);
+        vraw[r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
+      }
+      __syncthreads();
+      cp = vraw;
+    } else {
+      p = a.pivot ? cta_best(par).i : j;
+      cp = colptr(p) + j;
     }
-    __syncthreads();
-    const int p = s_p;
-    const double *colp = a.M + (int64_t)p * a.ldm;
-    const int len = a.rows - j;
+    stamp(1);
 
-    // ---- 2. reflector (xLARFG) from column p, rows j.., identical in every CTA
+    // ---- reflector (xLARFG), recomputed by every warp with the same order -> identical bits
     double part = 0.0;
-    for (int r = j + 1 + threadIdx.x; r < a.rows; r += blockDim.x) {
-      double x = __ldcg(colp + r);
-      part = fma(x, x, part);
-    }
-    double xn2 = block_sum(part, red);
-    double alpha = __ldcg(colp + j);
-    double xnorm = sqrt(xn2);
+    for (int r = 1 + lane; r < len; r += 32) part = fma(cp[r], cp[r], part);
+    const double xn2 = warp_sum(part);
+    const double alpha = cp[0];
+    const double xnorm = sqrt(xn2);
     double tau, beta, scal;
     if (xnorm == 0.0) {
       tau = 0.0; beta = alpha; scal = 0.0;
@@ -167,54 +228,64 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int r = threadIdx.x; r < len; r += blockDim.x) v[r] = (r == 0) ? 1.0 : __ldcg(colp + j + r) * scal;
-    __syncthreads();
-    if (blockIdx.x == 0) {
-      double *vs = a.Vst + (int64_t)j * a.rows;
-      for (int r = threadIdx.x; r < a.rows; r += blockDim.x) vs[r] = (r < j) ? 0.0 : v[r - j];
-      if (threadIdx.x == 0) { a.tau[j] = tau; a.beta[j] = beta; a.perm[j] = p; }
+    if (b == 0 && warp == 0) {
+      double *vs = a.Vst + (int64_t)j * rows;
+      for (int r = lane; r < rows; r += 32) vs[r] = (r < j) ? 0.0 : (r == j ? 1.0 : cp[r - j] * scal);
+      if (lane == 0) { a.tau[j] = tau; a.beta[j] = beta; a.perm[j] = p; }
     }
+    const int ob = p % G;
+    if (b == ob && threadIdx.x == 0) {
+      done_l[p / G] = 1;
+      a.done[p] = 1;
+    }
+    stamp(2);
 
-    // ---- 3. apply H_j to every owned, not yet pivoted column; downdate its norm
+    // ---- apply H_j (v = [1; cp[1..] scal]) to every owned, not yet pivoted column; downdate
     best = Best{-1.0, 0x7fffffff};
-    for (int i = gw; i < a.cols; i += W) {
-      if (i == p) {
-        if (lane == 0) a.done[i] = 1;
-        continue;
-      }
-      if (a.done[i]) continue;
-      double *col = a.M + (int64_t)i * a.ldm + j;
+    for (int li = warp; li < nown; li += wpb) {
+      const int gi = b + li * G;
+      if (gi == p || done_l[li]) continue;
+      double *col = colptr(li) + j;
       if (tau != 0.0) {
-        double w = 0.0;
-        for (int r = lane; r < len; r += 32) w = fma(v[r], col[r], w);
+        double w = lane == 0 ? col[0] : 0.0;
+        for (int r = 1 + lane; r < len; r += 32) w = fma(cp[r] * scal, col[r], w);
         w = warp_sum(w) * tau;
-        for (int r = lane; r < len; r += 32) col[r] = fma(-w, v[r], col[r]);
+        if (lane == 0) col[0] -= w;
+        for (int r = 1 + lane; r < len; r += 32) col[r] = fma(-w, cp[r] * scal, col[r]);
         __syncwarp();
       }
       if (a.pivot) {
-        double n1 = a.vn1[i];
+        double n1 = vn1[li];
         if (n1 != 0.0) {
           double t = __ddiv_rn(fabs(col[0]), n1);
           t = __dsub_rn(1.0, __dmul_rn(t, t));
           t = t < 0.0 ? 0.0 : t;
-          double rr = __ddiv_rn(n1, a.vn2[i]);
-          double t2 = __dmul_rn(__dmul_rn(t, rr), rr);
+          const double rr = __ddiv_rn(n1, vn2[li]);
+          const double t2 = __dmul_rn(__dmul_rn(t, rr), rr);
           if (t2 <= TOL3Z) {
-            if (j + 1 < a.rows) n1 = warp_norm(col + 1, len - 1);
-            else n1 = 0.0;
-            if (lane == 0) a.vn2[i] = n1;
+            n1 = (j + 1 < rows) ? warp_norm(col + 1, len - 1) : 0.0;
+            if (lane == 0) vn2[li] = n1;
           } else {
             n1 = __dmul_rn(n1, __dsqrt_rn(t));
           }
           __syncwarp();
-          if (lane == 0) a.vn1[i] = n1;
+          if (lane == 0) vn1[li] = n1;
         }
-        if (better(n1, i, best.v, best.i)) { best.v = n1; best.i = i; }
+        if (better(n1, gi, best.v, best.i)) { best.v = n1; best.i = gi; }
       }
     }
-    publish();
-    grid_sync(bcount, bgen);
+    {
+      Best wb = warp_best(best);
+      if (lane == 0) { s_bv[par ^ 1][warp] = wb.v; s_bi[par ^ 1][warp] = wb.i; }
+    }
+    __syncthreads();
+    stamp(3);
+    if (GRID && warp == 0 && j + 1 < a.steps) publish(j + 1, cta_best(par ^ 1));
   }
+  __syncthreads();
+  if (SMEMC)
+    for (int li = 0; li < nown; ++li)
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) a.M[(int64_t)(b + li * G) * a.ldm + r] = colbuf[(int64_t)li * rows + r];
 }
 
 // perm[steps..cols) = not-pivoted columns in ascending original order (single CTA scan).
@@ -262,27 +333,41 @@ __global__ void extract_r_kernel(int steps, int cols, const double *M, int64_t l
   }
 }
 
-// Explicit Q(:, t) = H_0 .. H_t e_t (xORG2R), one warp per column, then signed by sign(beta_t).
+// Explicit Q(:, t) = H_0 .. H_t e_t (xORG2R), one warp per column kept in shared memory, then
+// signed by sign(beta_t).  The reflectors are staged in shared memory when they fit.
+template <bool VSMEM>
 __global__ void form_q_kernel(int rows, int steps, const double *Vst, const double *tau, const double *beta,
                               double *Q, int64_t ldq) {
-  const int lane = threadIdx.x & 31;
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < steps; t += W) {
-    double *q = Q + (int64_t)t * ldq;
+  extern __shared__ double fsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *vs = fsm;
+  double *q = fsm + (VSMEM ? (int64_t)rows * steps : 0) + (int64_t)warp * rows;
+  __shared__ double taus[1056];
+  const int tmax = min(steps, (int)((blockIdx.x + 1) * nw * 1));  // unused guard
+  (void)tmax;
+  if (VSMEM)
+    for (int64_t e = threadIdx.x; e < (int64_t)rows * steps; e += blockDim.x) vs[e] = Vst[e];
+  for (int e = threadIdx.x; e < steps && e < 1056; e += blockDim.x) taus[e] = tau[e];
+  __syncthreads();
+  const double *V = VSMEM ? vs : Vst;
+  const int W = gridDim.x * nw;
+  for (int t = blockIdx.x * nw + warp; t < steps; t += W) {
     for (int r = lane; r < rows; r += 32) q[r] = (r == t) ? 1.0 : 0.0;
     __syncwarp();
     for (int j = t; j >= 0; --j) {
-      double tj = tau[j];
+      const double tj = taus[j];
       if (tj == 0.0) continue;
-      const double *v = Vst + (int64_t)j * rows;
+      const double *v = V + (int64_t)j * rows;
       double w = 0.0;
       for (int r = j + lane; r < rows; r += 32) w = fma(v[r], q[r], w);
       w = warp_sum(w) * tj;
       for (int r = j + lane; r < rows; r += 32) q[r] = fma(-w, v[r], q[r]);
       __syncwarp();
     }
-    if (beta[t] < 0.0)
-      for (int r = lane; r < rows; r += 32) q[r] = -q[r];
+    const double sg = beta[t] < 0.0 ? -1.0 : 1.0;
+    double *out = Q + (int64_t)t * ldq;
+    for (int r = lane; r < rows; r += 32) out[r] = sg * q[r];
+    __syncwarp();
   }
 }
 
@@ -297,44 +382,67 @@ void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms) {
   int64_t steps = std::min(rows, cols);
   s.max_rows = rows;
   s.max_cols = cols;
-  s.max_slots = (int64_t)num_sms * 8;
+  s.max_slots = num_sms;
   s.Vst = a.take<double>(rows * steps);
   s.tau = a.take<double>(steps);
   s.beta = a.take<double>(steps);
-  s.vn1 = a.take<double>(cols);
-  s.vn2 = a.take<double>(cols);
-  s.slot_val = a.take<double>(s.max_slots);
-  s.slot_idx = a.take<int>(s.max_slots);
+  s.rec = a.take<unsigned long long>(2 * s.max_slots * 4);
+  s.cand = a.take<unsigned long long>(2 * s.max_slots * rows * 2);
   s.done = a.take<int>(cols);
   s.perm = a.take<int64_t>(cols);
 }
 
+template <bool GRID, bool SMEMC>
+static void set_engine_attr() {
+  static bool done = false;
+  if (!done) {
+    RQLP_CUDA(cudaFuncSetAttribute(hh_engine_kernel<GRID, SMEMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   220 * 1024));
+    done = true;
+  }
+}
+
 void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot) {
   if (rows > s.max_rows || cols > s.max_cols) throw std::runtime_error("hh_factor: scratch too small");
+  constexpr size_t SMEM_MAX = 220 * 1024;
   EngineArgs a;
   a.M = M; a.ldm = ldm; a.rows = (int)rows; a.cols = (int)cols;
   a.steps = (int)std::min(rows, cols); a.pivot = pivot ? 1 : 0;
-  a.Vst = s.Vst; a.tau = s.tau; a.beta = s.beta; a.vn1 = s.vn1; a.vn2 = s.vn2;
-  a.slot_val = s.slot_val; a.slot_idx = s.slot_idx; a.done = s.done; a.perm = s.perm;
-  a.bar = c.dflags + BAR_COUNT;
-  size_t smem = (size_t)(rows + 32) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    RQLP_CUDA(cudaFuncSetAttribute(hh_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
-  if (smem > 200 * 1024) throw std::runtime_error("hh_factor: too many rows for the shared reflector buffer");
-  RQLP_CUDA(cudaMemsetAsync(c.dflags + BAR_COUNT, 0, sizeof(unsigned), c.stream));
-  if (cols <= 2048) {
-    hh_engine_kernel<<<1, 1024, smem, c.stream>>>(a);
+  a.Vst = s.Vst; a.tau = s.tau; a.beta = s.beta; a.rec = s.rec; a.cand = s.cand; a.done = s.done; a.perm = s.perm;
+  a.epoch = 0;
+  a.trace = c.trace;
+  auto smem_for = [&](int64_t owned, bool cached) {
+    return (size_t)(rows + 2 * owned + (cached ? owned * rows : 0)) * 8 + (size_t)owned * 4 + 64;
+  };
+  if (smem_for(cols, true) <= SMEM_MAX) {
+    // whole matrix in one CTA's shared memory: no global exchange at all
+    a.owned_max = (int)cols;
+    set_engine_attr<false, true>();
+    hh_engine_kernel<false, true><<<1, 1024, smem_for(cols, true), c.stream>>>(a);
     RQLP_LAUNCHED(c);
   } else {
-    int per_sm = 0;
-    RQLP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hh_engine_kernel, 256, smem));
-    int grid = std::max(1, std::min(per_sm, 4)) * c.num_sms;
-    grid = std::min<int64_t>(grid, s.max_slots);
+    const int G = (int)std::min<int64_t>(c.num_sms, s.max_slots);
+    const int64_t owned = ceil_div(cols, G);
+    const bool cached = smem_for(owned, true) <= SMEM_MAX;
+    if (!cached && smem_for(owned, false) > SMEM_MAX) throw std::runtime_error("hh_factor: too many rows");
+    a.owned_max = (int)owned;
+    const size_t smem = smem_for(owned, cached);
+    static unsigned epoch = 0;
+    epoch = (epoch + 1) & 0xffffu;
+    if (epoch == 0) {  // wrapped: clear stale tags once
+      RQLP_CUDA(cudaMemsetAsync(s.rec, 0, sizeof(unsigned long long) * 2 * G * 4, c.stream));
+      RQLP_CUDA(cudaMemsetAsync(s.cand, 0, sizeof(unsigned long long) * 2 * G * rows * 2, c.stream));
+      epoch = 1;
+    }
+    a.epoch = epoch;
     void *args[] = {&a};
-    RQLP_CUDA(cudaLaunchCooperativeKernel((void *)hh_engine_kernel, grid, 256, args, smem, c.stream));
+    if (cached) {
+      set_engine_attr<true, true>();
+      RQLP_CUDA(cudaLaunchCooperativeKernel((void *)hh_engine_kernel<true, true>, G, 512, args, smem, c.stream));
+    } else {
+      set_engine_attr<true, false>();
+      RQLP_CUDA(cudaLaunchCooperativeKernel((void *)hh_engine_kernel<true, false>, G, 512, args, smem, c.stream));
+    }
     RQLP_LAUNCHED(c);
   }
   if (cols > a.steps) {
@@ -355,8 +463,22 @@ void hh_extract_r(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, const double
 
 void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq) {
   int64_t steps = std::min(rows, cols);
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(steps * 32, 256), (int64_t)c.num_sms * 8));
-  form_q_kernel<<<grid, 256, 0, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q, ldq);
+  if (steps > 1056) throw std::runtime_error("hh_form_q: more than 1056 reflectors");
+  const int nw = 8;
+  const size_t vbytes = (size_t)rows * steps * 8, qbytes = (size_t)nw * rows * 8;
+  static bool attr = false;
+  if (!attr) {
+    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(steps, nw), (int64_t)c.num_sms));
+  if (vbytes + qbytes <= 190 * 1024) {
+    form_q_kernel<true><<<grid, nw * 32, vbytes + qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q,
+                                                                     ldq);
+  } else {
+    form_q_kernel<false><<<grid, nw * 32, qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q, ldq);
+  }
   RQLP_LAUNCHED(c);
 }
 

@@ -63,6 +63,7 @@ struct Ctx {
   void *comm = nullptr;
   int rank = 0, nranks = 1;
   int64_t collectives = 0;
+  unsigned long long *trace = nullptr;  // debug: engine phase timestamps
 };
 
 // ---- NCCL (comm.cu) ----
@@ -127,8 +128,9 @@ void orth(Ctx &ctx, OrthScratch &s, int64_t m, int64_t c, const double *Y, int64
 // ---- Householder engine + QLP tail (householder.cu, tail.cu) ----
 struct HHScratch {
   double *Vst = nullptr;        // rows x steps reflector store
-  double *tau = nullptr, *beta = nullptr, *vn1 = nullptr, *vn2 = nullptr, *slot_val = nullptr;
-  int *done = nullptr, *slot_idx = nullptr;
+  double *tau = nullptr, *beta = nullptr;
+  unsigned long long *rec = nullptr, *cand = nullptr;
+  int *done = nullptr;
   int64_t *perm = nullptr;
   int64_t max_rows = 0, max_cols = 0, max_slots = 0;
 };

@@ -11,6 +11,13 @@
 // R19).  A Cholesky pivot d_j <= 1e-12 G_jj (cond(Y) >~ 1e6) switches the pass to the shifted
 // Gram G + s I, s = 11 (m c + c (c+1)) u ||Y||_F^2, and enables a third pass (sCholQR3).  All of
 // this is decided on the device (no host sync): the conditional kernels read a flag word.
+//
+// The c x c Cholesky factor R and its inverse X = R^-1 come from one kernel: Gaussian
+// elimination of [G | I] in registers (c <= 128), one __syncthreads per pivot step:
+//   step k:  S_ij -= S_ik S_jk / d_k  (k < j <= i),   W_ik = -S_ik / d_k,  W_it -= (S_ik/d_k) W_kt,
+// after which L = S D^-1/2 (G = L L^T, R = L^T) and L^-1 = D^-1/2 W, X = (L^-1)^T.
+// Larger c is blocked by 128 with the diagonal blocks done by the same kernel and the panels
+// and block back-substitution done by GEMMs.
 #include "internal.cuh"
 
 namespace rqlpk {
@@ -23,74 +30,134 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
 
 namespace {
 
-constexpr int CHOL_NB = 128;          // diagonal block handled in shared memory
+constexpr int CHOL_SMALL = 128;       // largest c done in one CTA (4 x 32 register rows)
+constexpr int CHOL_NB = 128;          // diagonal block of the blocked path
 constexpr double CHOL_BREAK = 1e-12;  // relative pivot threshold for the shifted fallback
 
-// Cholesky G = R^T R of one nb x nb diagonal block in shared memory (right-looking, upper R).
-// Gorig gives the original diagonal for the relative breakdown test.  On breakdown sets
-// fail_word |= fail_bit and leaves R undefined.  Skipped unless (*cond & mask) (when cond set).
-__global__ void __launch_bounds__(1024) chol_block_kernel(int nb, double *G, int64_t ldg, const double *Gorig,
-                                                          int64_t ldo, double *R, int64_t ldr, unsigned *fail_word,
-                                                          unsigned fail_bit, const unsigned *cond,
-                                                          unsigned cond_mask) {
+// One CTA: R (upper, G = R^T R) and X = R^-1 (upper) of the n x n SPD block G (n <= 128).
+// Gorig supplies the original diagonal for the relative breakdown test.  On breakdown sets
+// (*fail_word) |= fail_bit (R, X then undefined).  Skipped unless (*cond & mask) when cond set.
+//
+// The working matrix M (n x n) holds S (Schur complements) in its lower triangle and W^T in its
+// strictly upper triangle (M[t][i] = W_it, t < i; W unit lower).  Thread (c, q) (c = column,
+// q = row quarter) keeps M[32q .. 32q+31][c] in registers.  Step k needs only column k of M
+// (bc[r] = M[r][k], bc[k] := 1) and d_k = M[k][k]; every active element updates as
+//     x -= bc[r] bc[c] / d_k     active iff c > k and (r >= c or r <= k),
+// except W_ck (r == k) which becomes -bc[c]/d_k (covered by bc[k] = 1 because its old value is 0).
+// Inactive elements get a zero multiplier (branch-free); warps whose columns are all <= k retire
+// from the step.  The owners of column k+1 publish it right after their step-k update, so a
+// step costs a single __syncthreads.
+__global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G, int64_t ldg, const double *Gorig,
+                                                          int64_t ldo, double *R, int64_t ldr, double *X, int64_t ldx,
+                                                          unsigned *fail_word, unsigned fail_bit,
+                                                          const unsigned *cond, unsigned cond_mask) {
   if (cond && ((*cond) & cond_mask) == 0) return;
-  extern __shared__ double S[];  // nb x nb, col-major
+  extern __shared__ double xs[];  // n x (n|1) staging for the coalesced X write
+  __shared__ __align__(16) double bc[2][CHOL_SMALL];
+  __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL];
   __shared__ int s_fail;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int i = e % nb, j = e / nb;
-    S[e] = (i <= j) ? G[i + (int64_t)j * ldg] : 0.0;
+  const int c = threadIdx.x & (CHOL_SMALL - 1), q = threadIdx.x >> 7;  // 128 columns x 4 quarters
+  const int r0 = 32 * q;
+  const bool col_ok = c < n;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int r = r0 + i;
+    x[i] = (col_ok && r < n && r >= c) ? G[c + (int64_t)r * ldg] : 0.0;  // S = G (symmetric)
   }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) g0s[i] = Gorig[i + (int64_t)i * ldo];
   if (threadIdx.x == 0) s_fail = 0;
+  for (int i = threadIdx.x; i < 2 * CHOL_SMALL; i += blockDim.x) (&bc[0][0])[i] = 0.0;
   __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    if (threadIdx.x == 0) {
-      double d = S[j + j * nb];
-      double g0 = Gorig[j + (int64_t)j * ldo];
-      if (!(d > CHOL_BREAK * g0) || !isfinite(d)) {
-        s_fail = 1;
-        d = 1.0;
+  if (c == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = r0 + i;
+      if (r < n) bc[0][r] = (r == 0) ? 1.0 : x[i];
+      if (r == 0) {
+        double d = x[i];
+        if (!(d > CHOL_BREAK * g0s[0]) || !isfinite(d)) {
+          s_fail = 1;
+          d = 1.0;
+        }
+        dpiv[0] = d;
+        dinv[0] = 1.0 / d;
       }
-      S[j + j * nb] = sqrt(d);
     }
-    __syncthreads();
-    double djj = S[j + j * nb];
-    for (int cix = j + 1 + threadIdx.x; cix < nb; cix += blockDim.x) S[j + cix * nb] /= djj;
-    __syncthreads();
-    int t = nb - j - 1;
-    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
-      int r = j + 1 + e % t, cix = j + 1 + e / t;
-      if (r <= cix) S[r + cix * nb] = fma(-S[j + r * nb], S[j + cix * nb], S[r + cix * nb]);
+  }
+  __syncthreads();
+  const unsigned rowvalid = (n - r0 >= 32) ? 0xffffffffu : (n - r0 <= 0 ? 0u : ((1u << (n - r0)) - 1u));
+  for (int k = 0; k < n; ++k) {
+    const double *b0 = bc[k & 1];
+    double *b1 = bc[(k + 1) & 1];
+    const int warp_c0 = (threadIdx.x & 127) - (threadIdx.x & 31);  // first column of this warp
+    if (warp_c0 + 31 > k && warp_c0 < n) {
+      const double bcc = (col_ok && c > k) ? b0[c] * dinv[k] : 0.0;
+      // active rows: r <= k (W part) or r >= c (S part)
+      const int lo_cnt = min(max(k - r0 + 1, 0), 32);               // rows r0 .. k
+      const int hi_start = min(max(c - r0, 0), 32);                 // rows c .. r0+31
+      const unsigned lowm = lo_cnt >= 32 ? 0xffffffffu : ((1u << lo_cnt) - 1u);
+      const unsigned highm = hi_start >= 32 ? 0u : (0xffffffffu << hi_start);
+      const unsigned act = (lowm | highm) & rowvalid;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const double2 br = *reinterpret_cast<const double2 *>(b0 + r0 + i);
+        const double m0 = ((act >> i) & 1u) ? bcc : 0.0;
+        const double m1 = ((act >> (i + 1)) & 1u) ? bcc : 0.0;
+        x[i] = fma(-br.x, m0, x[i]);
+        x[i + 1] = fma(-br.y, m1, x[i + 1]);
+      }
+    }
+    // publish column k+1 (and its pivot d, breakdown-checked, and 1/d)
+    const int kn = k + 1;
+    if (kn < n && c == kn) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 2)
+        *reinterpret_cast<double2 *>(b1 + r0 + i) = make_double2(x[i], x[i + 1]);
+      if (kn >= r0 && kn < r0 + 32) {
+        double d = b1[kn];
+        if (!(d > CHOL_BREAK * g0s[kn]) || !isfinite(d)) {
+          s_fail = 1;
+          d = 1.0;
+        }
+        dpiv[kn] = d;
+        dinv[kn] = 1.0 / d;
+        b1[kn] = 1.0;
+      }
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int i = e % nb, j = e / nb;
-    R[i + (int64_t)j * ldr] = (i <= j) ? S[e] : 0.0;
+  __syncthreads();
+  // outputs: R(c, r) = S_rc / sqrt(d_c) (r > c), R(r, r) = sqrt(d_r), R lower = 0;
+  //          X(r, c) = W_cr / sqrt(d_c) (r < c), X(r, r) = 1 / sqrt(d_r), X lower = 0.
+  const int ldxs = n | 1;
+  if (col_ok) {
+    const double sdc = sqrt(dpiv[c]);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = r0 + i;
+      if (r >= n) continue;
+      if (r > c) {
+        R[c + (int64_t)r * ldr] = x[i] / sdc;  // coalesced over c
+        xs[r + c * ldxs] = 0.0;
+      } else if (r == c) {
+        R[c + (int64_t)c * ldr] = sdc;
+        xs[c + c * ldxs] = 1.0 / sdc;
+      } else {
+        xs[r + c * ldxs] = x[i] / sdc;
+      }
+    }
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    if (i > j) R[i + (int64_t)j * ldr] = 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    X[i + (int64_t)j * ldx] = xs[i + j * ldxs];
   }
   if (threadIdx.x == 0 && s_fail) atomicOr(fail_word, fail_bit);
-}
-
-// X = R^-1 (upper triangular n x n), one warp per column by back substitution.
-__global__ void trtri_upper_kernel(int n, const double *R, int64_t ldr, double *X, int64_t ldx, const unsigned *cond,
-                                   unsigned cond_mask) {
-  if (cond && ((*cond) & cond_mask) == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int W = (gridDim.x * blockDim.x) >> 5;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += W) {
-    double *x = X + (int64_t)t * ldx;
-    for (int r = lane; r < n; r += 32) x[r] = 0.0;
-    __syncwarp();
-    if (lane == 0) x[t] = 1.0 / R[t + (int64_t)t * ldr];
-    __syncwarp();
-    for (int i = t - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1 + lane; k <= t; k += 32) s = fma(R[i + (int64_t)k * ldr], x[k], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) x[i] = -s / R[i + (int64_t)i * ldr];
-      __syncwarp();
-    }
-  }
 }
 
 // G2 += s I with s = 11 (m c + c(c+1)) u tr(G2); run only if (*cond & mask).  Marks the
@@ -117,37 +184,58 @@ __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsign
   }
 }
 
-}  // namespace
-
-// Cholesky of the c x c Gram G (destroyed) into upper R, blocked by CHOL_NB, with breakdown
-// reported in (*cond_word) |= fail_bit.  Gorig holds the original diagonal.  All kernels run only
-// if (*cond & mask) when cond is given.
-static void chol_attempt(Ctx &c, int64_t n, double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
-                         int64_t ldr, double *Xb, unsigned *fail_word, unsigned fail_bit, const unsigned *cond,
-                         unsigned mask, double *partials, size_t partial_elems) {
+void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
+                     int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
+                     const unsigned *cond, unsigned mask) {
   static bool attr = false;
   if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CHOL_NB * CHOL_NB * 8 + 1024));
+    RQLP_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   CHOL_SMALL * (CHOL_SMALL | 1) * 8));
     attr = true;
   }
+  chol_inv_kernel<<<1, 512, (size_t)n * (n | 1) * 8, c.stream>>>(n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word,
+                                                                 fail_bit, cond, mask);
+  RQLP_LAUNCHED(c);
+}
+
+}  // namespace
+
+// Cholesky G = R^T R (G destroyed) and X = R^-1, both n x n upper; breakdown reported as
+// (*fail_word) |= fail_bit.  Gorig holds the original diagonal.  All kernels run only if
+// (*cond & mask) when cond is given.
+static void chol_inv(Ctx &c, int64_t n, double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
+                     int64_t ldr, double *X, int64_t ldx, double *T, unsigned *fail_word, unsigned fail_bit,
+                     const unsigned *cond, unsigned mask, double *partials, size_t partial_elems) {
+  if (n <= CHOL_SMALL) {
+    launch_chol_inv(c, (int)n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, cond, mask);
+    return;
+  }
+  // blocked right-looking Cholesky with 128-wide diagonal blocks
   for (int64_t jb = 0; jb < n; jb += CHOL_NB) {
-    int b = (int)std::min<int64_t>(CHOL_NB, n - jb);
-    chol_block_kernel<<<1, 1024, (size_t)b * b * 8, c.stream>>>(b, G + jb + jb * ldg, ldg, Gorig + jb + jb * ldo, ldo,
-                                                                R + jb + jb * ldr, ldr, fail_word, fail_bit, cond, mask);
-    RQLP_LAUNCHED(c);
+    int64_t b = std::min<int64_t>(CHOL_NB, n - jb);
+    launch_chol_inv(c, (int)b, G + jb + jb * ldg, ldg, Gorig + jb + jb * ldo, ldo, R + jb + jb * ldr, ldr,
+                    X + jb + jb * ldx, ldx, fail_word, fail_bit, cond, mask);
     int64_t rest = n - jb - b;
     if (rest > 0) {
-      trtri_upper_kernel<<<(b + 7) / 8, 256, 0, c.stream>>>(b, R + jb + jb * ldr, ldr, Xb, CHOL_NB, cond, mask);
-      RQLP_LAUNCHED(c);
-      // R12 = R11^-T G12
-      gemm_generic_ex(c, true, false, b, rest, b, 1.0, Xb, CHOL_NB, G + jb + (jb + b) * ldg, ldg, 0.0,
+      // R12 = R11^-T G12 ; G22 -= R12^T R12 ; zero the lower blocks of R and X
+      gemm_generic_ex(c, true, false, b, rest, b, 1.0, X + jb + jb * ldx, ldx, G + jb + (jb + b) * ldg, ldg, 0.0,
                       R + jb + (jb + b) * ldr, ldr, partials, partial_elems, false, cond, mask);
-      // G22 -= R12^T R12
-      gemm_generic_ex(c, true, false, rest, rest, b, -1.0, R + jb + (jb + b) * ldr, ldr, R + jb + (jb + b) * ldr,
-                      ldr, 1.0, G + (jb + b) + (jb + b) * ldg, ldg, partials, partial_elems, false, cond, mask);
-      // zero the strictly lower block of R
+      gemm_generic_ex(c, true, false, rest, rest, b, -1.0, R + jb + (jb + b) * ldr, ldr, R + jb + (jb + b) * ldr, ldr,
+                      1.0, G + (jb + b) + (jb + b) * ldg, ldg, partials, partial_elems, false, cond, mask);
       launch_copy(c, rest, b, nullptr, 0, R + (jb + b) + jb * ldr, ldr, false, cond, mask);
+      launch_copy(c, rest, b, nullptr, 0, X + (jb + b) + jb * ldx, ldx, false, cond, mask);
+    }
+  }
+  // off-diagonal blocks of X = R^-1 by block back substitution:
+  //   X_IJ = -X_II (R_{I, I+1..J} X_{I+1..J, J}),  I = J-1 .. 0
+  for (int64_t J = CHOL_NB; J < n; J += CHOL_NB) {
+    int64_t bJ = std::min<int64_t>(CHOL_NB, n - J);
+    for (int64_t I = J - CHOL_NB; I >= 0; I -= CHOL_NB) {
+      int64_t k0 = I + CHOL_NB, kw = J + bJ - k0;
+      gemm_generic_ex(c, false, false, CHOL_NB, bJ, kw, 1.0, R + I + k0 * ldr, ldr, X + k0 + J * ldx, ldx, 0.0, T,
+                      CHOL_NB, partials, partial_elems, false, cond, mask);
+      gemm_generic_ex(c, false, false, CHOL_NB, bJ, CHOL_NB, -1.0, X + I + I * ldx, ldx, T, CHOL_NB, 0.0,
+                      X + I + J * ldx, ldx, partials, partial_elems, false, cond, mask);
     }
   }
 }
@@ -159,7 +247,7 @@ void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms) {
   s.R = a.take<double>(lc * c);
   s.Rinv = a.take<double>(lc * c);
   s.Racc = a.take<double>(lc * c);
-  s.tmp = a.take<double>(std::max<int64_t>(lc * c, CHOL_NB * CHOL_NB));
+  s.tmp = a.take<double>(std::max<int64_t>(lc * c, CHOL_NB * lc));
   s.ldy = round_up(m, 8);
   s.Ybuf = a.take<double>(s.ldy * c);
   s.partial_elems = std::max(gemm_partials_needed(m, c, c, num_sms), (size_t)std::max<int64_t>(4 * lc * c, 1));
@@ -177,16 +265,15 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask);
   if (sharded) allreduce_sum(c, s.G, lc * n);   // Gram summed over the row shards
   launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);
-  chol_attempt(c, n, s.G, lc, s.G2, lc, Rout, lc, s.tmp, condw, pass_bit, cond, mask, s.partials, s.partial_elems);
+  chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
+           s.partial_elems);
   // breakdown -> shifted Gram from the saved copy, second attempt (only if pass_bit was set)
   add_shift_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G2, lc, (double)m, c.dflags + FLAG_WORD, condw, pass_bit,
                                              pass_bit << 8);
   RQLP_LAUNCHED(c);
   launch_copy(c, n, n, s.G2, lc, s.G, lc, false, condw, pass_bit);
-  chol_attempt(c, n, s.G, lc, s.G2, lc, Rout, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials, s.partial_elems);
-  trtri_upper_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (int64_t)c.num_sms * 4)), 256, 0,
-                       c.stream>>>((int)n, Rout, lc, s.Rinv, lc, cond, mask);
-  RQLP_LAUNCHED(c);
+  chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
+           s.partial_elems);
   gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, cond, mask);
 }
 

@@ -112,10 +112,10 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
     double *Pspare = s.tmp_nl;
     double *Rcur = s.Rhat;
     for (int i = 2; i <= d; ++i) {
+      // [Q^(i), R^(i)] = qr([R^(i-1)]^T): unpivoted, so CholeskyQR2 gives the same unique
+      // factors (R_ii > 0) as Householder to rounding (reading R3).
       launch_copy(c, l, l, Rcur, ldl, s.Mt, ldl, true);      // [R^(i-1)]^T
-      hh_factor(c, s.hh, l, l, s.Mt, ldl, false);
-      hh_extract_r(c, s.hh, l, l, s.Mt, ldl, s.Lt, ldl, false);  // R^(i)
-      hh_form_q(c, s.hh, l, l, s.Qt, ldl);                       // Q^(i)
+      orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, s.Lt, ldl, false);
       if (i % 2 == 0) {
         gemm_generic_ex(c, false, false, l, l, l, 1.0, s.QE, ldl, s.Qt, ldl, 0.0, s.tmp_ll, ldl, s.orth.partials,
                         s.orth.partial_elems, false, nullptr, 0);
