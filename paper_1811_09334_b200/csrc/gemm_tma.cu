@@ -241,18 +241,22 @@ int choose_bn(int64_t c) {
   return best;
 }
 
-// Split-K: minimise waves(T) * ceil(ktiles / S) with T = tiles * S CTAs (1 CTA per SM).
-int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems) {
+// Split-K: minimise the modelled time  waves(T) * ceil(ktiles / S) * t_ktile
+//                                      + (S > 1) * (2 S M N 8 bytes / HBM + reduce launch)
+// with T = tiles * S CTAs (1 CTA per SM), t_ktile = 128 BN 24 2 flop / (DMMA peak per SM).
+int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems, int bn) {
+  const double t_ktile = 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);   // s
+  const double hbm = 6.0e12;                                           // B/s
   int best = 1;
-  double best_cost = 1e300;
+  double best_t = 1e300;
   for (int s = 1; s <= 64; ++s) {
     if (s > 1 && (size_t)s * out_elems > partial_cap_elems) break;
     if (s > 1 && ktiles / s < 4) break;
-    int64_t T = tiles * s;
-    double waves = (double)ceil_div(T, num_sms);
-    double cost = waves * (double)ceil_div(ktiles, s) + (s > 1 ? 0.02 * ktiles + 2.0 : 0.0);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
+    const int64_t T = tiles * s;
+    double t = (double)ceil_div(T, num_sms) * (double)ceil_div(ktiles, s) * t_ktile;
+    if (s > 1) t += 2.0 * s * (double)out_elems * 8.0 / hbm + 4e-6;
+    if (t < best_t * 0.995) {
+      best_t = t;
       best = s;
     }
   }
@@ -313,7 +317,7 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
     int64_t M = mode == 0 ? m : k, K = mode == 0 ? k : m;
     int bn = choose_bn(cc);
     int64_t tiles = ceil_div(M, BM) * ceil_div(cc, bn);
-    int S = choose_splits(tiles, ceil_div(K, BK), num_sms, (size_t)1 << 62, M * cc);
+    int S = choose_splits(tiles, ceil_div(K, BK), num_sms, (size_t)1 << 62, M * cc, bn);
     if (S > 1) best = std::max(best, (size_t)S * M * cc);
   }
   return best;
@@ -329,7 +333,7 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (!make_map(&mb, X, k, cc, ldx, BK, bn)) return false;
   int64_t ktiles = ceil_div(k, BK);
   int64_t tiles = ceil_div(m, BM) * ceil_div(cc, bn);
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn);
   dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask);
   return true;
 }
@@ -344,7 +348,7 @@ bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (!make_map(&mb, V, m, cc, ldv, BK, bn)) return false;
   int64_t ktiles = ceil_div(m, BK);
   int64_t tiles = ceil_div(k, BM) * ceil_div(cc, bn);
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn);
   dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask);
   return true;
 }
