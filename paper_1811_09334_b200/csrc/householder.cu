@@ -59,6 +59,12 @@ __device__ double block_sum(double s, double *red) {
   return warp_sum(t);
 }
 
+__device__ double warp_sumsq(const double *x, int64_t len) {
+  double s = 0.0;
+  for (int64_t r = threadIdx.x & 31; r < len; r += 32) s = fma(x[r], x[r], s);
+  return warp_sum(s);
+}
+
 __device__ double warp_norm(const double *x, int64_t len) {
   double s = 0.0;
   for (int64_t r = threadIdx.x & 31; r < len; r += 32) s = fma(x[r], x[r], s);
@@ -93,7 +99,7 @@ __device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
 // downdates their norms; warps post their best candidate in a parity-double-buffered slot and
 // meet at the step's single __syncthreads; every warp then reduces the 32 slots itself.
 template <bool GRID, bool SMEMC>
-__global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs a) {
   extern __shared__ double smem[];
   double *vraw = smem;
   double *vn1 = vraw + a.rows;
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
   Best best{-1.0, 0x7fffffff};
   if (a.pivot)
     for (int li = warp; li < nown; li += wpb) {
-      double nrm = warp_norm(colptr(li), rows);
+      double nrm = warp_sumsq(colptr(li), rows);  // squared norms (monotone: same argmax)
       if (lane == 0) { vn1[li] = nrm; vn2[li] = nrm; }
       if (better(nrm, b + li * G, best.v, best.i)) { best.v = nrm; best.i = b + li * G; }
     }
@@ -181,16 +187,32 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
       if (warp == 0) {
         Best c{-1.0, 0x7fffffff};
         if (a.pivot) {
-          for (int s = lane; s < G; s += 32) {
-            volatile unsigned long long *rc = a.rec + ((int64_t)par * G + s) * 4;
-            unsigned long long w0, w1, w2;
-            do {
-              w0 = rc[0]; w1 = rc[1]; w2 = rc[2];
-            } while ((unsigned)w0 != tag || (unsigned)w1 != tag || (unsigned)w2 != tag);
-            const double val = __longlong_as_double((long long)(((w0 >> 32) << 32) | (w1 >> 32)));
-            const int idx = (int)(w2 >> 32);
-            if (better(val, idx, c.v, c.i)) { c.v = val; c.i = idx; }
+          // each lane owns records lane, lane+32, ...: issue all loads, re-poll only the stale ones
+          constexpr int MAXR = 8;  // G <= 256
+          unsigned long long w0[MAXR], w1[MAXR], w2[MAXR];
+          unsigned pending = 0;
+#pragma unroll
+          for (int t = 0; t < MAXR; ++t)
+            if (lane + 32 * t < G) pending |= 1u << t;
+          while (pending) {
+#pragma unroll
+            for (int t = 0; t < MAXR; ++t)
+              if (pending & (1u << t)) {
+                volatile unsigned long long *rc = a.rec + ((int64_t)par * G + lane + 32 * t) * 4;
+                w0[t] = rc[0]; w1[t] = rc[1]; w2[t] = rc[2];
+              }
+#pragma unroll
+            for (int t = 0; t < MAXR; ++t)
+              if ((pending & (1u << t)) && (unsigned)w0[t] == tag && (unsigned)w1[t] == tag && (unsigned)w2[t] == tag)
+                pending &= ~(1u << t);
           }
+#pragma unroll
+          for (int t = 0; t < MAXR; ++t)
+            if (lane + 32 * t < G) {
+              const double val = __longlong_as_double((long long)(((w0[t] >> 32) << 32) | (w1[t] >> 32)));
+              const int idx = (int)(w2[t] >> 32);
+              if (better(val, idx, c.v, c.i)) { c.v = val; c.i = idx; }
+            }
           c = warp_best(c);
         } else {
           c.i = j;
@@ -202,8 +224,10 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
       volatile const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * rows * 2;
       for (int r = threadIdx.x; r < len; r += blockDim.x) {
         unsigned long long lo, hi;
-        do { lo = src[2 * r]; } while ((unsigned)lo != tag);
-        do { hi = src[2 * r + 1]; } while ((unsigned)hi != tag);
+        do {
+          lo = src[2 * r];
+          hi = src[2 * r + 1];
+        } while ((unsigned)lo != tag || (unsigned)hi != tag);
         vraw[r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
       }
       __syncthreads();
@@ -219,12 +243,11 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
     for (int r = 1 + lane; r < len; r += 32) part = fma(cp[r], cp[r], part);
     const double xn2 = warp_sum(part);
     const double alpha = cp[0];
-    const double xnorm = sqrt(xn2);
     double tau, beta, scal;
-    if (xnorm == 0.0) {
+    if (xn2 == 0.0) {
       tau = 0.0; beta = alpha; scal = 0.0;
     } else {
-      beta = -copysign(sqrt(alpha * alpha + xnorm * xnorm), alpha);
+      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
@@ -255,18 +278,19 @@ __global__ void __launch_bounds__(1024) hh_engine_kernel(EngineArgs a) {
         __syncwarp();
       }
       if (a.pivot) {
+        // xLAQP2 downdating on squared norms (vn1 = ||.||^2, vn2 = ||.||^2 at the last
+        // recompute): t = 1 - (x/vn1)^2 = 1 - x^2/vn1sq, recompute when t vn1sq/vn2sq <= tol3z.
         double n1 = vn1[li];
         if (n1 != 0.0) {
-          double t = __ddiv_rn(fabs(col[0]), n1);
-          t = __dsub_rn(1.0, __dmul_rn(t, t));
+          const double x = col[0];
+          double t = 1.0 - (x * x) / n1;
           t = t < 0.0 ? 0.0 : t;
-          const double rr = __ddiv_rn(n1, vn2[li]);
-          const double t2 = __dmul_rn(__dmul_rn(t, rr), rr);
+          const double t2 = t * n1 / vn2[li];
           if (t2 <= TOL3Z) {
-            n1 = (j + 1 < rows) ? warp_norm(col + 1, len - 1) : 0.0;
+            n1 = (j + 1 < rows) ? warp_sumsq(col + 1, len - 1) : 0.0;
             if (lane == 0) vn2[li] = n1;
           } else {
-            n1 = __dmul_rn(n1, __dsqrt_rn(t));
+            n1 = n1 * t;
           }
           __syncwarp();
           if (lane == 0) vn1[li] = n1;
@@ -414,14 +438,15 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
   auto smem_for = [&](int64_t owned, bool cached) {
     return (size_t)(rows + 2 * owned + (cached ? owned * rows : 0)) * 8 + (size_t)owned * 4 + 64;
   };
-  if (smem_for(cols, true) <= SMEM_MAX) {
+  if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
     // whole matrix in one CTA's shared memory: no global exchange at all
     a.owned_max = (int)cols;
     set_engine_attr<false, true>();
     hh_engine_kernel<false, true><<<1, 1024, smem_for(cols, true), c.stream>>>(a);
     RQLP_LAUNCHED(c);
   } else {
-    const int G = (int)std::min<int64_t>(c.num_sms, s.max_slots);
+    // enough CTAs that each owns >= 8 columns (fewer records to exchange), at most one per SM
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(c.num_sms, s.max_slots), ceil_div(cols, 8)));
     const int64_t owned = ceil_div(cols, G);
     const bool cached = smem_for(owned, true) <= SMEM_MAX;
     if (!cached && smem_for(owned, false) > SMEM_MAX) throw std::runtime_error("hh_factor: too many rows");
