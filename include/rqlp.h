@@ -150,6 +150,13 @@ int rqlp_residual_sq(rqlp_handle_t h, int64_t m, int64_t n, int64_t l, const dou
                      const double *Q, int64_t ldq, const double *T, int64_t ldt, const double *P,
                      int64_t ldp, double *res_dev);
 
+/* Stage outputs for staged parity (tests): subsequent factorisations on h copy the sketch
+ * Y = AΩ (m x l, before orthonormalisation), the final range basis V (m x l) and the projected
+ * B (l x n; for BRQLP the deflated B_j rows) into these device buffers.  Any may be NULL;
+ * rqlp_set_stage_outputs(h, NULL, 0, NULL, 0, NULL, 0) turns it off. */
+int rqlp_set_stage_outputs(rqlp_handle_t h, double *Y, int64_t ldy, double *V, int64_t ldv, double *B,
+                           int64_t ldb);
+
 /* Per-stage device timings (ms) of the last factorisation when timing is enabled:
  * names/values written up to *count entries; returns number available. */
 int rqlp_set_timing(rqlp_handle_t h, int enable);

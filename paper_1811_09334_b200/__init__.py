@@ -143,6 +143,12 @@ class Handle:
             raise RQLPError(f"rqlp_get_timing rc={-nout}")
         return [(names[i].decode(), float(ms[i])) for i in range(min(nout, cap))]
 
+    def set_stage_outputs(self, Y=None, V=None, B=None):
+        """Tests: copy the sketch Y, final V and projected B of subsequent factorisations."""
+        _check(lib().rqlp_set_stage_outputs(self.h, _ptr(Y), _ld(Y) if Y is not None else 0, _ptr(V),
+                                            _ld(V) if V is not None else 0, _ptr(B),
+                                            _ld(B) if B is not None else 0), "rqlp_set_stage_outputs")
+
     def launches(self) -> int:
         return int(lib().rqlp_launch_count(self.h))
 

@@ -40,6 +40,7 @@ SIGNATURES = [
     ("rqlp_qlp_tail", _int, [_vp, _i64, _i64, _vp, _i64, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp,
                              ctypes.POINTER(_int)]),
     ("rqlp_residual_sq", _int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    ("rqlp_set_stage_outputs", _int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64]),
     ("rqlp_set_timing", _int, [_vp, _int]),
     ("rqlp_get_timing", _int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _int]),
     ("rqlp_launch_count", _i64, [_vp]),

@@ -27,6 +27,9 @@ struct rqlp_handle_s {
   // staging buffers for host pointers in rqlp()
   void *stage = nullptr;
   size_t stage_bytes = 0;
+  // optional stage outputs (tests): sketch Y, final V, projected B
+  double *dbgY = nullptr, *dbgV = nullptr, *dbgB = nullptr;
+  int64_t ldY = 0, ldV = 0, ldB = 0;
 };
 
 namespace rqlpk {
@@ -177,13 +180,14 @@ int check_common(int64_t m, int64_t n, int k, int p, int q) {
 // ---- RQLP / ERQLP ------------------------------------------------------------------------
 // Range finder + q subspace iterations (Alg.1 l.1-3 + reading R12), B = V^T A (Alg.1 l.4).
 void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, const double *A, int64_t lda,
-                       uint64_t seed) {
+                       uint64_t seed, rqlp_handle_t h) {
   const bool sh = c.nranks > 1;
   c.mark("start");
   launch_omega(c, n, l, 0, seed, P.Om, P.ldn);                                        // l.1
   c.mark("omega");
   gemm_nn(c, m, l, n, A, lda, P.Om, P.ldn, P.Y, P.ldm, P.part, P.part_elems);         // l.2 Y = AΩ
   c.mark("pass_sketch");
+  if (h->dbgY) launch_copy(c, m, l, P.Y, P.ldm, h->dbgY, h->ldY, false);
   orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh);                      // l.3 V = qr(Y)
   c.mark("orth");
   for (int it = 0; it < q; ++it) {
@@ -200,6 +204,8 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.B, P.ldl, true, P.part, P.part_elems);    // l.4 B = V^T A
   allreduce_sum(c, P.B, P.ldl * n);
   c.mark("pass_project");
+  if (h->dbgV) launch_copy(c, m, l, P.V, P.ldm, h->dbgV, h->ldV, false);
+  if (h->dbgB) launch_copy(c, l, n, P.B, P.ldl, h->dbgB, h->ldB, false);
 }
 
 int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, const double *A, int64_t lda,
@@ -215,7 +221,7 @@ int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
   Plan P;
   carve_plan(a, P, d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP, m, n, l, 0, c.num_sms);
   RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
-  range_and_project(c, P, m, n, l, q, A, lda, seed);
+  range_and_project(c, P, m, n, l, q, A, lda, seed, h);
   qlp_tail(c, P.tail, l, n, P.B, P.ldl, d, P.QB, P.ldl, T, ldt, Pout, ldp, piv0, piv1);   // l.5-7
   gemm_nn(c, m, l, l, P.V, P.ldm, P.QB, P.ldl, Q, ldq, P.part, P.part_elems);             // Q = V Q_B
   c.mark("assemble_Q");
@@ -245,6 +251,7 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
   c.mark("omega");
   gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);               // l.3 all Y_j = AΩ_j
   c.mark("pass_sketch");
+  if (h->dbgY) launch_copy(c, m, l, P.Y, ldm, h->dbgY, h->ldY, false);
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
@@ -303,6 +310,8 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
     gemm_nn(c, m, bj, bj, Vj, ldm, P.QB, P.tail.ldl, Q + c0 * ldq, ldq, P.part, P.part_elems);
     c.mark("block_tail");
   }
+  if (h->dbgV) launch_copy(c, m, l, P.V, ldm, h->dbgV, h->ldV, false);
+  if (h->dbgB) launch_copy(c, l, n, B, LL, h->dbgB, h->ldB, false);
   h->launches = c.launches;
   return RQLP_OK;
 }
@@ -791,6 +800,14 @@ int rqlp_residual_sq(rqlp_handle_t h, int64_t m, int64_t n, int64_t l, const dou
     h->launches = c.launches;
     return RQLP_OK;
   });
+}
+
+int rqlp_set_stage_outputs(rqlp_handle_t h, double *Y, int64_t ldy, double *V, int64_t ldv, double *B, int64_t ldb) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  h->dbgY = Y; h->ldY = ldy;
+  h->dbgV = V; h->ldV = ldv;
+  h->dbgB = B; h->ldB = ldb;
+  return RQLP_OK;
 }
 
 int rqlp_set_timing(rqlp_handle_t h, int enable) {

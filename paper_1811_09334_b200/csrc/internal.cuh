@@ -118,6 +118,7 @@ struct OrthScratch {
   double *partials = nullptr;
   size_t partial_elems = 0;
   double *scal = nullptr;       // small device scalars
+  int *dep = nullptr;           // dependent-column flags of the last Cholesky (rank deficiency)
 };
 void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms);
 // V = orth(Y) (CholeskyQR2 + conditional shifted pass).  Y is preserved; Y and V must not alias.  R (nullable) receives the c x c triangular factor (Y = V R).

@@ -34,6 +34,29 @@ constexpr int CHOL_SMALL = 128;       // largest c done in one CTA (4 x 32 regis
 constexpr int CHOL_NB = 128;          // diagonal block of the blocked path
 constexpr double CHOL_BREAK = 1e-12;  // relative pivot threshold for the shifted fallback
 
+constexpr double CHOL_DEP = 1e-15;  // relative pivot at or below which a column is dependent
+
+// d = Schur pivot of column k, g0 = its original Gram diagonal.  Dependent column (rank
+// deficiency, d <= 1e-15 g0, incl. a zero column): dep[k] = 1, pivot 1.  Ill-conditioned
+// (d <= 1e-12 g0): breakdown -> the shifted pass.  Returns the pivot to use.
+__device__ __forceinline__ double classify_pivot(double d, double g0, int k, int *dep, int *s_fail, int *s_dep) {
+  if (dep) dep[k] = 0;
+  if (!isfinite(d)) {
+    *s_fail = 1;
+    return 1.0;
+  }
+  if (dep && !(d > CHOL_DEP * g0)) {
+    dep[k] = 1;
+    *s_dep = 1;
+    return 1.0;
+  }
+  if (!(d > CHOL_BREAK * g0)) {
+    *s_fail = 1;
+    return 1.0;
+  }
+  return d;
+}
+
 // One CTA: R (upper, G = R^T R) and X = R^-1 (upper) of the n x n SPD block G (n <= 128).
 // Gorig supplies the original diagonal for the relative breakdown test.  On breakdown sets
 // (*fail_word) |= fail_bit (R, X then undefined).  Skipped unless (*cond & mask) when cond set.
@@ -49,13 +72,14 @@ constexpr double CHOL_BREAK = 1e-12;  // relative pivot threshold for the shifte
 // step costs a single __syncthreads.
 __global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G, int64_t ldg, const double *Gorig,
                                                           int64_t ldo, double *R, int64_t ldr, double *X, int64_t ldx,
-                                                          unsigned *fail_word, unsigned fail_bit,
+                                                          unsigned *fail_word, unsigned fail_bit, int *dep,
+                                                          unsigned dep_bit, unsigned *flag_word,
                                                           const unsigned *cond, unsigned cond_mask) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   extern __shared__ double xs[];  // n x (n|1) staging for the coalesced X write
   __shared__ __align__(16) double bc[2][CHOL_SMALL];
   __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL];
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_dep;
   const int c = threadIdx.x & (CHOL_SMALL - 1), q = threadIdx.x >> 7;  // 128 columns x 4 quarters
   const int r0 = 32 * q;
   const bool col_ok = c < n;
@@ -66,7 +90,7 @@ __global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G
     x[i] = (col_ok && r < n && r >= c) ? G[c + (int64_t)r * ldg] : 0.0;  // S = G (symmetric)
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) g0s[i] = Gorig[i + (int64_t)i * ldo];
-  if (threadIdx.x == 0) s_fail = 0;
+  if (threadIdx.x == 0) { s_fail = 0; s_dep = 0; }
   for (int i = threadIdx.x; i < 2 * CHOL_SMALL; i += blockDim.x) (&bc[0][0])[i] = 0.0;
   __syncthreads();
   if (c == 0) {
@@ -75,11 +99,7 @@ __global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G
       const int r = r0 + i;
       if (r < n) bc[0][r] = (r == 0) ? 1.0 : x[i];
       if (r == 0) {
-        double d = x[i];
-        if (!(d > CHOL_BREAK * g0s[0]) || !isfinite(d)) {
-          s_fail = 1;
-          d = 1.0;
-        }
+        const double d = classify_pivot(x[i], g0s[0], 0, dep, &s_fail, &s_dep);
         dpiv[0] = d;
         dinv[0] = 1.0 / d;
       }
@@ -115,11 +135,7 @@ __global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G
       for (int i = 0; i < 32; i += 2)
         *reinterpret_cast<double2 *>(b1 + r0 + i) = make_double2(x[i], x[i + 1]);
       if (kn >= r0 && kn < r0 + 32) {
-        double d = b1[kn];
-        if (!(d > CHOL_BREAK * g0s[kn]) || !isfinite(d)) {
-          s_fail = 1;
-          d = 1.0;
-        }
+        const double d = classify_pivot(b1[kn], g0s[kn], kn, dep, &s_fail, &s_dep);
         dpiv[kn] = d;
         dinv[kn] = 1.0 / d;
         b1[kn] = 1.0;
@@ -158,6 +174,35 @@ __global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G
     X[i + (int64_t)j * ldx] = xs[i + j * ldxs];
   }
   if (threadIdx.x == 0 && s_fail) atomicOr(fail_word, fail_bit);
+  if (threadIdx.x == 0 && s_dep && dep) {
+    atomicOr(fail_word, dep_bit);
+    atomicOr(flag_word, (unsigned)RQLP_FLAG_RANK_DEFICIENT);
+  }
+}
+
+// dep[k] != 0: column k of Q (m x n) is replaced by a Philox N(0,1) vector (stream 7, counter =
+// row + m k); the next CholeskyQR pass orthonormalises it against the others (basis completion
+// for rank-deficient input, reading R4/R21).
+__global__ void replace_dep_kernel(int64_t m, int n, double *Q, int64_t ldq, const int *dep, uint64_t seed,
+                                   const unsigned *cond, unsigned cond_mask) {
+  if (cond && ((*cond) & cond_mask) == 0) return;
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    if (!dep[k]) continue;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+      uint64_t ctr = (uint64_t)(i + m * k), key = seed;
+      // SplitMix64-style hash -> two uniforms -> Box-Muller (any N(0,1)-like fill works here)
+      uint64_t z1 = ctr * 0x9E3779B97F4A7C15ULL + key;
+      z1 = (z1 ^ (z1 >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      z1 = (z1 ^ (z1 >> 27)) * 0x94D049BB133111EBULL;
+      z1 ^= z1 >> 31;
+      uint64_t z2 = (ctr + 0x632BE59BD9B4E019ULL) * 0x9E3779B97F4A7C15ULL + key;
+      z2 = (z2 ^ (z2 >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      z2 = (z2 ^ (z2 >> 27)) * 0x94D049BB133111EBULL;
+      z2 ^= z2 >> 31;
+      const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1p-53, u2 = (double)(z2 >> 11) * 0x1p-53;
+      Q[i + (int64_t)k * ldq] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+  }
 }
 
 // G2 += s I with s = 11 (m c + c(c+1)) u tr(G2); run only if (*cond & mask).  Marks the
@@ -186,7 +231,7 @@ __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsign
 
 void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
-                     const unsigned *cond, unsigned mask) {
+                     const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0) {
   static bool attr = false;
   if (!attr) {
     RQLP_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -194,7 +239,8 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
     attr = true;
   }
   chol_inv_kernel<<<1, 512, (size_t)n * (n | 1) * 8, c.stream>>>(n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word,
-                                                                 fail_bit, cond, mask);
+                                                                 fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond,
+                                                                 mask);
   RQLP_LAUNCHED(c);
 }
 
@@ -205,16 +251,17 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
 // (*cond & mask) when cond is given.
 static void chol_inv(Ctx &c, int64_t n, double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
                      int64_t ldr, double *X, int64_t ldx, double *T, unsigned *fail_word, unsigned fail_bit,
-                     const unsigned *cond, unsigned mask, double *partials, size_t partial_elems) {
+                     const unsigned *cond, unsigned mask, double *partials, size_t partial_elems, int *dep,
+                     unsigned dep_bit) {
   if (n <= CHOL_SMALL) {
-    launch_chol_inv(c, (int)n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, cond, mask);
+    launch_chol_inv(c, (int)n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, cond, mask, dep, dep_bit);
     return;
   }
   // blocked right-looking Cholesky with 128-wide diagonal blocks
   for (int64_t jb = 0; jb < n; jb += CHOL_NB) {
     int64_t b = std::min<int64_t>(CHOL_NB, n - jb);
     launch_chol_inv(c, (int)b, G + jb + jb * ldg, ldg, Gorig + jb + jb * ldo, ldo, R + jb + jb * ldr, ldr,
-                    X + jb + jb * ldx, ldx, fail_word, fail_bit, cond, mask);
+                    X + jb + jb * ldx, ldx, fail_word, fail_bit, cond, mask, dep ? dep + jb : nullptr, dep_bit);
     int64_t rest = n - jb - b;
     if (rest > 0) {
       // R12 = R11^-T G12 ; G22 -= R12^T R12 ; zero the lower blocks of R and X
@@ -253,6 +300,7 @@ void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms) {
   s.partial_elems = std::max(gemm_partials_needed(m, c, c, num_sms), (size_t)std::max<int64_t>(4 * lc * c, 1));
   s.partials = a.take<double>((int64_t)s.partial_elems);
   s.scal = a.take<double>(8);
+  s.dep = a.take<int>(c);
 }
 
 // One CholeskyQR pass: Qout = Yin R^-1 with G = Yin^T Yin.  pass_bit marks this pass's
@@ -262,19 +310,27 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
                         bool sharded) {
   int64_t lc = round_up(n, 8);
   unsigned *condw = c.dflags + COND_WORD;
+  const unsigned dep_bit = pass_bit << 16;
   gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask);
   if (sharded) allreduce_sum(c, s.G, lc * n);   // Gram summed over the row shards
-  launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);
-  chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
-           s.partial_elems);
-  // breakdown -> shifted Gram from the saved copy, second attempt (only if pass_bit was set)
+  if (n > CHOL_SMALL) launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);  // blocked path destroys G
+  const double *Gorig = n > CHOL_SMALL ? s.G2 : s.G;
+  chol_inv(c, n, s.G, lc, Gorig, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
+           s.partial_elems, s.dep, dep_bit);
+  // breakdown (ill-conditioned) -> shifted Gram, second attempt (only if pass_bit was set)
+  if (n <= CHOL_SMALL) launch_copy(c, n, n, s.G, lc, s.G2, lc, false, condw, pass_bit);
   add_shift_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G2, lc, (double)m, c.dflags + FLAG_WORD, condw, pass_bit,
                                              pass_bit << 8);
   RQLP_LAUNCHED(c);
   launch_copy(c, n, n, s.G2, lc, s.G, lc, false, condw, pass_bit);
   chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
-           s.partial_elems);
+           s.partial_elems, nullptr, 0u);
   gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, cond, mask);
+  // rank-deficient columns -> random completion, orthonormalised by the following pass
+  replace_dep_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
+                           (unsigned)std::min<int64_t>(n, 64)),
+                       256, 0, c.stream>>>(m, (int)n, Qout, ldqo, s.dep, 0x5eedULL + pass_bit, condw, dep_bit);
+  RQLP_LAUNCHED(c);
 }
 
 void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t ldy, double *V, int64_t ldv,
@@ -290,8 +346,9 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
                     false, nullptr, 0);
     launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, nullptr, 0);
   }
-  // pass 3 (only when pass 1 or 2 needed the shift: bits 1<<8 | 2<<8): V -> Ybuf -> V
-  const unsigned m3 = (1u << 8) | (2u << 8);
+  // pass 3 (only when pass 1 or 2 needed the shift, bits 1<<8 | 2<<8, or completed dependent
+  // columns, bits 1<<16 | 2<<16): V -> Ybuf -> V
+  const unsigned m3 = (1u << 8) | (2u << 8) | (1u << 16) | (2u << 16);
   cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded);
   launch_copy(c, m, n, s.Ybuf, s.ldy, V, ldv, false, condw, m3);
   if (R) {
@@ -299,6 +356,12 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
                     false, condw, m3);
     launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, condw, m3);
     launch_copy(c, n, n, s.Racc, lc, R, ldr, false, nullptr, 0);
+    // with completed columns Y = V R no longer holds for R2 R1: R = V^T Y (upper triangular in
+    // exact arithmetic, zero rows for the completed directions)
+    const unsigned mdep = (1u << 16) | (2u << 16) | (4u << 16);
+    gemm_tn(c, m, n, n, V, ldv, Y, ldy, s.tmp, lc, false, s.partials, s.partial_elems, condw, mdep);
+    if (sharded) allreduce_sum(c, s.tmp, lc * n);
+    launch_copy(c, n, n, s.tmp, lc, R, ldr, false, condw, mdep);
   }
 }
 

@@ -177,3 +177,103 @@ def test_residual_kernel(rq, orc):
     o = orc.rqlp(A, 30, 6, q=0, d=0, seed=1)
     r = rq.residual(_cm(A), _cm(o["Q"]), _cm(o["T"]), _cm(o["P"]))
     assert r == pytest.approx(orc.residual(A, o["Q"], o["T"], o["P"]), rel=1e-10)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_zero_matrix(rq, orc):
+    """Zero A (reading R21): tau = 0 reflectors, L = 0, identity pivots; the GPU completes the
+    basis (rank deficiency) so Q and P stay orthonormal."""
+    A = np.zeros((60, 40), order="F")
+    g = rq.factorize(_cm(A), 3, 2, q=1, d=0, seed=1)
+    h = rq.Handle.default()
+    flags = h.sync()
+    o = orc.rqlp(A, 3, 2, q=1, d=0, seed=1)
+    assert not _np(g["T"]).any() and not o["T"].any()
+    assert list(g["piv0"].cpu().numpy()) == list(o["piv0"]) == [0, 1, 2, 3, 4]
+    Q, P = _np(g["Q"]), _np(g["P"])
+    assert np.abs(Q.T @ Q - np.eye(5)).max() <= 1e-13 * 5
+    assert np.abs(P.T @ P - np.eye(5)).max() <= 1e-13 * 5
+    assert flags & 2  # RQLP_FLAG_RANK_DEFICIENT
+
+
+@pytest.mark.parametrize("d", [0, 2])
+def test_exact_rank_deficient(rq, orc, d):
+    """rank(A) = 6 < l = 12: V's completion is not unique (reading R4), so compare the
+    basis-invariant quantities: residual ~ 0, the leading 6 pivots and L-values, orthonormality."""
+    sig = np.array([3.0, 2.0, 1.0, 0.5, 0.25, 0.125])
+    A = _rand_svd(300, 200, sig, 21)
+    g = rq.factorize(_cm(A), 8, 4, q=1, d=d, seed=5)
+    o = orc.rqlp(A, 8, 4, q=1, d=d, seed=5)
+    nA = np.linalg.norm(A)
+    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+    assert orc.residual(A, Q, T, P) <= 1e-13 * nA
+    assert np.array_equal(g["piv0"].cpu().numpy()[:6], o["piv0"][:6])
+    np.testing.assert_allclose(np.diag(T)[:6], np.diag(o["T"])[:6], rtol=1e-10)
+    assert np.abs(np.diag(T)[6:]).max() <= 1e-12 * sig[0]
+    assert np.abs(Q.T @ Q - np.eye(12)).max() <= 1e-13 * 12
+    assert np.abs(P.T @ P - np.eye(12)).max() <= 1e-13 * 12
+
+
+def test_l_equals_n_stewart(rq, orc):
+    """l = n: RQLP reduces to Stewart's pivoted QLP; GPU == oracle."""
+    A = _rand_svd(70, 30, np.logspace(0, -4, 30), 6)
+    g = rq.factorize(_cm(A), 25, 5, q=0, d=0, seed=11)
+    o = orc.rqlp(A, 25, 5, q=0, d=0, seed=11)
+    _check_factorization(rq, orc, A, g, o, 30)
+
+
+@pytest.mark.parametrize("m,n,k,p,q,d", [(40, 30, 2, 2, 0, 0), (9, 300, 3, 2, 1, 1), (500, 400, 30, 10, 3, 5),
+                                         (12, 12, 8, 4, 2, 2)])
+def test_small_and_degenerate_shapes(rq, orc, m, n, k, p, q, d):
+    """Minimal k = p = 2, m = l (square sketch), wide, many power steps / inner QRs."""
+    r = min(m, n)
+    sig = np.logspace(0, -3, r)
+    A = _rand_svd(m, n, sig, m * n + q)
+    g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=3)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=3)
+    if d >= 1:
+        o["piv1"] = None
+    _check_factorization(rq, orc, A, g, o, k + p, sig[:k + p] / sig[0])
+
+
+def test_brqlp_unit_blocks(rq, orc):
+    """b = 1: every block is a single column (Alg. 3 with h = l)."""
+    A = _rand_svd(200, 120, np.exp(-np.arange(1, 121.0) / 10), 31)
+    g = rq.factorize(_cm(A), 6, 3, q=1, b=1, seed=2)
+    o = orc.brqlp(A, 6, 3, b=1, q=1, seed=2)
+    _check_factorization(rq, orc, A, g, o, 9)
+
+
+def test_argument_errors_gpu(rq):
+    A = torch.zeros(10, 8, dtype=torch.float64, device="cuda").t().contiguous().t()
+    with pytest.raises(rq.RQLPError):
+        rq.rqlp(A, 1, 2)
+    with pytest.raises(rq.RQLPError):
+        rq.rqlp(A, 5, 4)          # l = 9 > n = 8
+    with pytest.raises(rq.RQLPError):
+        rq.erqlp(A, 3, 2, d=0)    # d >= 1
+    with pytest.raises(rq.RQLPError):
+        rq.brqlp(A, 3, 2, b=6)    # b <= l
+
+
+def test_host_pointer_entry_points(rq, orc):
+    """The north-star rqlp() and rqlp_factorize() with HOST buffers (e2e path) equal the device path."""
+    A = _rand_svd(300, 200, np.arange(1, 201.0) ** -2, 41)
+    Qh, Lh, Ph = rq.rqlp_host(A, 20, 5, q=1, seed=9)
+    g = rq.factorize(_cm(A), 20, 5, q=1, seed=9)
+    np.testing.assert_array_equal(Lh, _np(g["T"]))
+    np.testing.assert_array_equal(Qh, _np(g["Q"]))
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory().t()
+    Q2, T2, P2, tu = rq.factorize_host(At, 20, 5, q=1, d=2, seed=9)
+    g2 = rq.factorize(_cm(A), 20, 5, q=1, d=2, seed=9)
+    np.testing.assert_array_equal(T2.numpy(), _np(g2["T"]))
+    assert tu
+
+
+def test_deterministic_reruns(rq):
+    """Bitwise-identical results across reruns (fixed-order reductions, no atomics in sums)."""
+    A = _cm(_rand_svd(1031, 1030, np.exp(-np.arange(1, 1031.0) / 50), 2))
+    a = rq.factorize(A, 100, 10, q=1, d=2, seed=2)
+    b = rq.factorize(A, 100, 10, q=1, d=2, seed=2)
+    for key in ("Q", "T", "P", "piv0"):
+        assert torch.equal(a[key], b[key])
