@@ -84,17 +84,10 @@ class Handle:
             self.rank, self.nranks = 0, 1
         else:
             import torch.distributed as dist
+
+            from .dist import exchange_unique_id
             self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
-            uid = torch.zeros(128, dtype=torch.uint8)
-            if self.rank == 0:
-                buf = ctypes.create_string_buffer(128)
-                _check(lib().rqlp_get_unique_id(buf), "rqlp_get_unique_id")
-                uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
-            bdev = self.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
-            uid = uid.to(bdev)
-            dist.broadcast(uid, src=dist.get_global_rank(group, 0) if hasattr(dist, "get_global_rank") else 0,
-                           group=group)
-            raw = ctypes.create_string_buffer(bytes(uid.cpu().tolist()), 128)
+            raw = ctypes.create_string_buffer(exchange_unique_id(group), 128)
             _check(lib().rqlp_create_dist(ctypes.byref(h), self.device.index,
                                           ctypes.c_void_p(self.stream.cuda_stream), raw, self.rank, self.nranks),
                    "rqlp_create_dist")

@@ -181,7 +181,7 @@ int check_common(int64_t m, int64_t n, int k, int p, int q) {
 // Range finder + q subspace iterations (Alg.1 l.1-3 + reading R12), B = V^T A (Alg.1 l.4).
 void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, const double *A, int64_t lda,
                        uint64_t seed, rqlp_handle_t h) {
-  const bool sh = c.nranks > 1;
+  const bool sh = c.comm != nullptr;  // row-sharded handle: Grams are summed over ranks
   c.mark("start");
   launch_omega(c, n, l, 0, seed, P.Om, P.ldn);                                        // l.1
   c.mark("omega");
@@ -237,7 +237,7 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
   int64_t l = (int64_t)k + p;
   Ctx c = make_ctx(h);
   reset_timing(h);
-  const bool sh = c.nranks > 1;
+  const bool sh = c.comm != nullptr;  // row-sharded handle: Grams are summed over ranks
   size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l, b, c.num_sms);
   Arena a;
   a.base = get_ws(h, need, allow_own);
@@ -261,6 +261,7 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
     // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
     auto reorth = [&]() {
       if (c0 == 0) return;
+      c.mark("b_other");
       gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
       allreduce_sum(c, P.C, LL * bj);
       gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
@@ -271,8 +272,10 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
     orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
     reorth();                                                                            // l.5
     for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
+      c.mark("b_other");
       gemm_tn(c, m, bj, n, A, lda, Vj, ldm, P.Z, ldn, false, P.part, P.part_elems);     // Z = A^T Vj
       allreduce_sum(c, P.Z, ldn * bj);
+      c.mark("pass_block_AtV");
       if (c0 > 0) {
         gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems); // C = V_<j^T Vj
         allreduce_sum(c, P.C, LL * bj);
@@ -280,7 +283,9 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
                         nullptr, 0);                                                     // Z -= B_<j^T C
       }
       orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
+      c.mark("b_other");
       gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
+      c.mark("pass_block_AW");
       if (c0 > 0) {
         gemm_generic_ex(c, false, false, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems, false,
                         nullptr, 0);                                                     // D = B_<j W
@@ -293,8 +298,10 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
     // l.6: B_j = Vj^T A^(j-1) = Vj^T A - (Vj^T V_<j) B_<j, formed in the tail's B buffer
     double *Bj = P.tail.Bw;
     const int64_t ldbj = P.tail.ldl;
+    c.mark("b_other");
     gemm_tn(c, m, bj, n, A, lda, Vj, ldm, Bj, ldbj, true, P.part, P.part_elems);
     allreduce_sum(c, Bj, ldbj * n);
+    c.mark("pass_block_project");
     if (c0 > 0) {
       gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, LL, false, P.part, P.part_elems);    // E = Vj^T V_<j (bj x c0)
       allreduce_sum(c, P.D, LL * c0);
@@ -370,7 +377,7 @@ int rqlp_create_dist(rqlp_handle_t *out, int device, void *cuda_stream, const vo
   rqlp_handle_t h = *out;
   h->rank = rank;
   h->nranks = nranks;
-  if (nranks > 1) {
+  {  // a communicator even for nranks == 1 (the NCCL path is then exercised on one GPU)
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);

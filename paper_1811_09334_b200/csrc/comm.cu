@@ -86,7 +86,7 @@ void comm_destroy(void *comm) {
 
 // In-place sum over ranks of `count` doubles on the compute stream (ncclFloat64 = 8, ncclSum = 0).
 void allreduce_sum(Ctx &c, double *buf, int64_t count) {
-  if (c.nranks <= 1 || count <= 0) return;
+  if (!c.comm || count <= 0) return;
   nccl_check(g_nccl.allReduce(buf, buf, (size_t)count, 8, 0, (ncclComm_t)c.comm, c.stream), "ncclAllReduce");
   c.collectives++;
 }
