@@ -188,17 +188,18 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   gemm_nn(c, m, l, n, A, lda, P.Om, P.ldn, P.Y, P.ldm, P.part, P.part_elems);         // l.2 Y = AΩ
   c.mark("pass_sketch");
   if (h->dbgY) launch_copy(c, m, l, P.Y, P.ldm, h->dbgY, h->ldY, false);
-  orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh);                      // l.3 V = qr(Y)
+  // l.3 V = qr(Y); bases that only feed the next subspace-iteration product need just the span
+  orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh, q > 0);
   c.mark("orth");
   for (int it = 0; it < q; ++it) {
     gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.Z, P.ldn, false, P.part, P.part_elems); // Z = A^T V
     allreduce_sum(c, P.Z, P.ldn * l);
     c.mark("pass_power_AtV");
-    orth(c, P.orth, n, l, P.Z, P.ldn, P.W, P.ldn, nullptr, 0, false);                 // W = qr(Z)
+    orth(c, P.orth, n, l, P.Z, P.ldn, P.W, P.ldn, nullptr, 0, false, true);           // W = qr(Z) (span)
     c.mark("orth");
     gemm_nn(c, m, l, n, A, lda, P.W, P.ldn, P.Y, P.ldm, P.part, P.part_elems);        // Y = A W
     c.mark("pass_power_AW");
-    orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh);                    // V = qr(Y)
+    orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh, it + 1 < q);        // V = qr(Y)
     c.mark("orth");
   }
   gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.B, P.ldl, true, P.part, P.part_elems);    // l.4 B = V^T A

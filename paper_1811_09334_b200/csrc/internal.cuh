@@ -123,8 +123,10 @@ struct OrthScratch {
 void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms);
 // V = orth(Y) (CholeskyQR2 + conditional shifted pass).  Y is preserved; Y and V must not alias.  R (nullable) receives the c x c triangular factor (Y = V R).
 // sharded: Y is a row block of a row-sharded matrix -> the Gram is summed over ranks.
+// span_only: an intermediate subspace-iteration basis (one CholeskyQR pass; V spans range(Y) but
+// is only approximately orthonormal).
 void orth(Ctx &ctx, OrthScratch &s, int64_t m, int64_t c, const double *Y, int64_t ldy, double *V, int64_t ldv,
-          double *R, int64_t ldr, bool sharded = false);
+          double *R, int64_t ldr, bool sharded = false, bool span_only = false);
 
 // ---- Householder engine + QLP tail (householder.cu, tail.cu) ----
 struct HHScratch {

@@ -334,10 +334,16 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
 }
 
 void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t ldy, double *V, int64_t ldv,
-          double *R, int64_t ldr, bool sharded) {
+          double *R, int64_t ldr, bool sharded, bool span_only) {
   int64_t lc = round_up(n, 8);
   unsigned *condw = c.dflags + COND_WORD;
   RQLP_CUDA(cudaMemsetAsync(condw, 0, sizeof(unsigned), c.stream));
+  if (span_only && !R) {
+    // intermediate subspace-iteration basis: only range(V) = range(Y) matters (V = Y R^-1 for any
+    // invertible R keeps the span to the same O(u cond(Y)) rounding), so one CholeskyQR pass.
+    cholqr_pass(c, s, m, n, Y, ldy, V, ldv, s.Racc, 1u, nullptr, 0, sharded);
+    return;
+  }
   // pass 1: Y -> Ybuf (R1 in Racc), pass 2: Ybuf -> V (R2 in R)
   cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
   cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded);
