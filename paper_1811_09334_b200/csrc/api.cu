@@ -3,6 +3,7 @@
 // the method runs in this library's kernels on the handle's stream; the host only enqueues.
 #include <cuda.h>
 
+#include <map>
 #include <mutex>
 
 #include "internal.cuh"
@@ -30,6 +31,21 @@ struct rqlp_handle_s {
   // optional stage outputs (tests): sketch Y, final V, projected B
   double *dbgY = nullptr, *dbgV = nullptr, *dbgB = nullptr;
   int64_t ldY = 0, ldV = 0, ldB = 0;
+  // CUDA-graph cache: a factorisation is captured on its second call with the same shape,
+  // pointers and workspace, then replayed (one graph launch instead of ~100-300 kernel launches)
+  struct GEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> events;
+    std::vector<cudaEvent_t> pool;
+    int64_t launches = 0;
+  };
+  std::vector<cudaEvent_t> eager_pool;
+  std::map<std::string, GEntry> graphs;
+  std::map<std::string, int> seen;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
+  bool trace_free = getenv("RQLP_ENGINE_TRACE") == nullptr;
 };
 
 namespace rqlpk {
@@ -41,10 +57,11 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
                      size_t partial_elems, bool trans_out, const unsigned *cond, unsigned cond_mask);
 
 void Ctx::mark(const char *name) {
-  if (!timing || !events) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
-  cudaEventRecord(e, stream);
+  if (!timing || !events || !pool || pool_next >= pool->size()) return;
+  cudaEvent_t e = (*pool)[pool_next++];
+  // under capture an External record stays a timeable event node of the CUDA graph
+  if (capturing) cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+  else cudaEventRecord(e, stream);
   events->emplace_back(name, e);
 }
 
@@ -62,6 +79,7 @@ Ctx make_ctx(rqlp_handle_t h) {
   c.dflags = h->dflags;
   c.timing = h->timing;
   c.events = &h->events;
+  c.pool = &h->eager_pool;
   c.comm = h->comm;
   c.rank = h->rank;
   c.nranks = h->nranks;
@@ -72,9 +90,112 @@ Ctx make_ctx(rqlp_handle_t h) {
   return c;
 }
 
+constexpr int kEventPool = 512;
+
+void fill_pool(std::vector<cudaEvent_t> &pool) {
+  while ((int)pool.size() < kEventPool) {
+    cudaEvent_t e;
+    RQLP_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+}
+
 void reset_timing(rqlp_handle_t h) {
-  for (auto &e : h->events) cudaEventDestroy(e.second);
-  h->events.clear();
+  h->events.clear();  // events are owned by the pools
+  h->cur_events = &h->events;
+  if (h->timing) fill_pool(h->eager_pool);
+}
+
+bool graphs_enabled(rqlp_handle_t h) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("RQLP_GRAPHS");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && h->comm == nullptr && h->trace_free;
+}
+
+// Run `enqueue(Ctx&)` eagerly on the handle's stream, or -- from the second call with the same
+// key -- as a captured CUDA graph replayed on a handle-owned stream that is fenced to the caller's
+// stream with events (so the call stays asynchronous and stream-ordered for the caller).
+template <typename F>
+int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
+  if (!graphs_enabled(h)) {
+    Ctx c = make_ctx(h);
+    reset_timing(h);
+    enqueue(c);
+    h->launches = c.launches;
+    return RQLP_OK;
+  }
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end() && h->seen[key]++ == 0) {  // first call: eager (also warms static state)
+    Ctx c = make_ctx(h);
+    reset_timing(h);
+    enqueue(c);
+    h->launches = c.launches;
+    return RQLP_OK;
+  }
+  if (!h->gstream) {
+    RQLP_CUDA(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+  }
+  if (it == h->graphs.end()) {
+    rqlp_handle_s::GEntry e;
+    if (h->timing) fill_pool(e.pool);
+    Ctx c = make_ctx(h);
+    c.stream = h->gstream;
+    c.events = &e.events;
+    c.pool = &e.pool;
+    c.capturing = true;
+    cudaGraph_t g = nullptr;
+    RQLP_CUDA(cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue(c);
+    } catch (...) {
+      cudaStreamEndCapture(h->gstream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    RQLP_CUDA(cudaStreamEndCapture(h->gstream, &g));
+    cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    RQLP_CUDA(ie);
+    e.launches = c.launches;
+    if (h->graphs.size() >= 16) {  // small cache: drop everything when full
+      for (auto &kv : h->graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        for (auto ev : kv.second.pool) cudaEventDestroy(ev);
+      }
+      h->graphs.clear();
+    }
+    it = h->graphs.emplace(key, std::move(e)).first;
+  }
+  RQLP_CUDA(cudaEventRecord(h->ev_in, h->stream));
+  RQLP_CUDA(cudaStreamWaitEvent(h->gstream, h->ev_in, 0));
+  RQLP_CUDA(cudaGraphLaunch(it->second.exec, h->gstream));
+  RQLP_CUDA(cudaEventRecord(h->ev_out, h->gstream));
+  RQLP_CUDA(cudaStreamWaitEvent(h->stream, h->ev_out, 0));
+  h->cur_events = &it->second.events;
+  h->launches = it->second.launches;
+  return RQLP_OK;
+}
+
+std::string make_key(rqlp_handle_t h, const char *tag, std::initializer_list<int64_t> ints,
+                     std::initializer_list<const void *> ptrs) {
+  std::string k = tag;
+  char buf[40];
+  for (int64_t v : ints) {
+    snprintf(buf, sizeof buf, ",%lld", (long long)v);
+    k += buf;
+  }
+  for (const void *p : ptrs) {
+    snprintf(buf, sizeof buf, ",%p", p);
+    k += buf;
+  }
+  snprintf(buf, sizeof buf, ",t%d,s%p", h->timing ? 1 : 0, (void *)h->stream);
+  k += buf;
+  return k;
 }
 
 // ---- workspace plans ----------------------------------------------------------------------
@@ -212,36 +333,50 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
 int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, const double *A, int64_t lda,
              uint64_t seed, double *Q, int64_t ldq, double *T, int64_t ldt, double *Pout, int64_t ldp, int64_t *piv0,
              int64_t *piv1, bool allow_own) {
-  int64_t l = (int64_t)k + p;
-  Ctx c = make_ctx(h);
-  reset_timing(h);
-  size_t need = plan_bytes(d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP, m, n, l, 0, c.num_sms);
-  Arena a;
-  a.base = get_ws(h, need, allow_own);
-  a.cap = need;
-  Plan P;
-  carve_plan(a, P, d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP, m, n, l, 0, c.num_sms);
-  RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
-  range_and_project(c, P, m, n, l, q, A, lda, seed, h);
-  qlp_tail(c, P.tail, l, n, P.B, P.ldl, d, P.QB, P.ldl, T, ldt, Pout, ldp, piv0, piv1);   // l.5-7
-  gemm_nn(c, m, l, l, P.V, P.ldm, P.QB, P.ldl, Q, ldq, P.part, P.part_elems);             // Q = V Q_B
-  c.mark("assemble_Q");
-  h->launches = c.launches;
-  return RQLP_OK;
+  const int64_t l = (int64_t)k + p;
+  const int variant = d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP;
+  const size_t need = plan_bytes(variant, m, n, l, 0, h->num_sms);
+  char *ws = get_ws(h, need, allow_own);
+  const std::string key = make_key(h, "rqlp", {m, n, k, p, q, d, lda, (int64_t)seed, ldq, ldt, ldp, h->ldY, h->ldV, h->ldB},
+                                   {A, Q, T, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB});
+  return with_graph(h, key, [&](Ctx &c) {
+    Arena a;
+    a.base = ws;
+    a.cap = need;
+    Plan P;
+    carve_plan(a, P, variant, m, n, l, 0, c.num_sms);
+    RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+    range_and_project(c, P, m, n, l, q, A, lda, seed, h);
+    qlp_tail(c, P.tail, l, n, P.B, P.ldl, d, P.QB, P.ldl, T, ldt, Pout, ldp, piv0, piv1);   // l.5-7
+    gemm_nn(c, m, l, l, P.V, P.ldm, P.QB, P.ldl, Q, ldq, P.part, P.part_elems);             // Q = V Q_B
+    c.mark("assemble_Q");
+  });
 }
 
 // ---- BRQLP -------------------------------------------------------------------------------
+void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
+                   int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout,
+                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need);
 // Alg.3 with implicit deflation: A^(j-1) X = A X - V_<j (B_<j X), A^(j-1)^T V = A^T V - B_<j^T (V_<j^T V).
 int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A, int64_t lda,
               uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout, int64_t ldp, int64_t *piv0,
               int64_t *piv1, bool allow_own) {
-  int64_t l = (int64_t)k + p;
-  Ctx c = make_ctx(h);
-  reset_timing(h);
+  const int64_t l = (int64_t)k + p;
+  const size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l, b, h->num_sms);
+  char *ws = get_ws(h, need, allow_own);
+  const std::string key = make_key(h, "brqlp", {m, n, k, p, b, q, lda, (int64_t)seed, ldq, ldl, ldp, h->ldY, h->ldV, h->ldB},
+                                   {A, Q, L, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB});
+  return with_graph(h, key, [&](Ctx &c) { enqueue_brqlp(c, h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, Pout,
+                                                        ldp, piv0, piv1, ws, need); });
+}
+
+void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
+                   int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout,
+                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need) {
+  const int64_t l = (int64_t)k + p;
   const bool sh = c.comm != nullptr;  // row-sharded handle: Grams are summed over ranks
-  size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l, b, c.num_sms);
   Arena a;
-  a.base = get_ws(h, need, allow_own);
+  a.base = ws;
   a.cap = need;
   Plan P;
   carve_plan(a, P, RQLP_VARIANT_BRQLP, m, n, l, b, c.num_sms);
@@ -320,8 +455,6 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
   }
   if (h->dbgV) launch_copy(c, m, l, P.V, ldm, h->dbgV, h->ldV, false);
   if (h->dbgB) launch_copy(c, l, n, B, LL, h->dbgB, h->ldB, false);
-  h->launches = c.launches;
-  return RQLP_OK;
 }
 
 }  // namespace
@@ -403,6 +536,14 @@ int rqlp_destroy(rqlp_handle_t h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
   reset_timing(h);
+  for (auto &kv : h->graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    for (auto ev : kv.second.pool) cudaEventDestroy(ev);
+  }
+  for (auto ev : h->eager_pool) cudaEventDestroy(ev);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->own) cudaFree(h->own);
   if (h->stage) cudaFree(h->stage);
   if (h->dflags) cudaFree(h->dflags);
@@ -830,10 +971,12 @@ int rqlp_get_timing(rqlp_handle_t h, const char **names, float *ms, int capacity
     RQLP_CUDA(cudaStreamSynchronize(h->stream));
     h->names_out.clear();
     h->ms_out.clear();
-    for (size_t i = 1; i < h->events.size(); ++i) {
+    auto &ev = h->cur_events ? *h->cur_events : h->events;
+    RQLP_CUDA(cudaStreamSynchronize(h->gstream ? h->gstream : h->stream));
+    for (size_t i = 1; i < ev.size(); ++i) {
       float t = 0.f;
-      cudaEventElapsedTime(&t, h->events[i - 1].second, h->events[i].second);
-      h->names_out.push_back(h->events[i].first);
+      cudaEventElapsedTime(&t, ev[i - 1].second, ev[i].second);
+      h->names_out.push_back(ev[i].first);
       h->ms_out.push_back(t);
     }
     return RQLP_OK;

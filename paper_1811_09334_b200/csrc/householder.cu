@@ -80,7 +80,7 @@ struct EngineArgs {
   double *tau, *beta;
   unsigned long long *rec;   // [2][G][4] LL words: {hi(val)|tag, lo(val)|tag, idx|tag, -}
   unsigned long long *cand;  // [2][G][rows][2] LL words of the candidate column rows j.. (lo, hi halves)
-  unsigned epoch;            // high 16 bits of every tag (launch-unique, so stale words never match)
+  unsigned epoch;            // high 16 bits of every tag (0: the buffers are zeroed per launch)
   unsigned long long *trace; // optional per-step phase timestamps (CTA 0, thread 0), debugging only
   int *done;                // done[col] = 1 once pivoted (compaction of the non-pivot columns)
   int64_t *perm;
@@ -452,21 +452,29 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     if (!cached && smem_for(owned, false) > SMEM_MAX) throw std::runtime_error("hh_factor: too many rows");
     a.owned_max = (int)owned;
     const size_t smem = smem_for(owned, cached);
-    static unsigned epoch = 0;
-    epoch = (epoch + 1) & 0xffffu;
-    if (epoch == 0) {  // wrapped: clear stale tags once
-      RQLP_CUDA(cudaMemsetAsync(s.rec, 0, sizeof(unsigned long long) * 2 * G * 4, c.stream));
-      RQLP_CUDA(cudaMemsetAsync(s.cand, 0, sizeof(unsigned long long) * 2 * G * rows * 2, c.stream));
-      epoch = 1;
-    }
-    a.epoch = epoch;
-    void *args[] = {&a};
+    // zero the exchange buffers every launch: tags are then step+1 of THIS launch only (robust
+    // against recycled workspaces; a memset node when captured in a CUDA graph)
+    RQLP_CUDA(cudaMemsetAsync(s.rec, 0, sizeof(unsigned long long) * 2 * G * 4, c.stream));
+    RQLP_CUDA(cudaMemsetAsync(s.cand, 0, sizeof(unsigned long long) * 2 * G * rows * 2, c.stream));
+    a.epoch = 0;
+    // co-residency of all G CTAs is required (they exchange every step): cooperative launch
+    // through cudaLaunchKernelEx (capturable into CUDA graphs)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (cached) {
       set_engine_attr<true, true>();
-      RQLP_CUDA(cudaLaunchCooperativeKernel((void *)hh_engine_kernel<true, true>, G, 512, args, smem, c.stream));
+      RQLP_CUDA(cudaLaunchKernelEx(&cfg, hh_engine_kernel<true, true>, a));
     } else {
       set_engine_attr<true, false>();
-      RQLP_CUDA(cudaLaunchCooperativeKernel((void *)hh_engine_kernel<true, false>, G, 512, args, smem, c.stream));
+      RQLP_CUDA(cudaLaunchKernelEx(&cfg, hh_engine_kernel<true, false>, a));
     }
     RQLP_LAUNCHED(c);
   }

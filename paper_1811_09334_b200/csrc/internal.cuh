@@ -58,6 +58,9 @@ struct Ctx {
   unsigned *dflags = nullptr;     // NUM_DEV_FLAGS words of device memory
   bool timing = false;
   std::vector<std::pair<std::string, cudaEvent_t>> *events = nullptr;
+  std::vector<cudaEvent_t> *pool = nullptr;  // pre-created events (no cudaEventCreate under capture)
+  size_t pool_next = 0;
+  bool capturing = false;
   void mark(const char *name);
   // row-sharded runs (comm.cu): NCCL communicator, rank, number of ranks
   void *comm = nullptr;
