@@ -31,14 +31,26 @@ struct Best {
 };
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
 
+// Warp argmax (max value, lowest index on ties).  Values are >= 0 (squared norms) or -1 (no
+// candidate); non-negative doubles order like their bit patterns, so one redux.sync on the high
+// 32 bits (biased so -1 sorts lowest) narrows the candidates, usually to a single lane.
 __device__ __forceinline__ Best warp_best(Best b) {
+  const long long bits = __double_as_longlong(b.v);
+  const unsigned hi = b.v < 0.0 ? 0u : (unsigned)((unsigned long long)bits >> 32) + 1u;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  unsigned cand = __ballot_sync(0xffffffffu, hi == mhi);
+  if (__popc(cand) == 1) {
+    const int src = __ffs(cand) - 1;
+    return Best{__shfl_sync(0xffffffffu, b.v, src), __shfl_sync(0xffffffffu, b.i, src)};
+  }
+  Best c = (hi == mhi) ? b : Best{-1.0, 0x7fffffff};
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, b.v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, b.i, o);
-    if (better(ov, oi, b.v, b.i)) { b.v = ov; b.i = oi; }
+    double ov = __shfl_xor_sync(0xffffffffu, c.v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, c.i, o);
+    if (better(ov, oi, c.v, c.i)) { c.v = ov; c.i = oi; }
   }
-  return b;
+  return c;
 }
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -248,8 +260,10 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
       tau = 0.0; beta = alpha; scal = 0.0;
     } else {
       beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+      const double amb = alpha - beta;              // tau = (beta - alpha)/beta, scal = 1/(alpha - beta)
+      const double rinv = 1.0 / (beta * amb);       // one division for both
+      tau = -amb * amb * rinv;
+      scal = beta * rinv;
     }
     if (b == 0 && warp == 0) {
       double *vs = a.Vst + (int64_t)j * rows;
@@ -263,39 +277,52 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
     }
     stamp(2);
 
-    // ---- apply H_j (v = [1; cp[1..] scal]) to every owned, not yet pivoted column; downdate
+    // ---- apply H_j (v = [1; cp[1..] scal]) to every owned, not yet pivoted column; downdate.
+    //      8-lane groups: a warp updates 4 columns at once (3-step group reductions).
     best = Best{-1.0, 0x7fffffff};
-    for (int li = warp; li < nown; li += wpb) {
-      const int gi = b + li * G;
-      if (gi == p || done_l[li]) continue;
-      double *col = colptr(li) + j;
-      if (tau != 0.0) {
-        double w = lane == 0 ? col[0] : 0.0;
-        for (int r = 1 + lane; r < len; r += 32) w = fma(cp[r] * scal, col[r], w);
-        w = warp_sum(w) * tau;
-        if (lane == 0) col[0] -= w;
-        for (int r = 1 + lane; r < len; r += 32) col[r] = fma(-w, cp[r] * scal, col[r]);
-        __syncwarp();
-      }
-      if (a.pivot) {
-        // xLAQP2 downdating on squared norms (vn1 = ||.||^2, vn2 = ||.||^2 at the last
-        // recompute): t = 1 - (x/vn1)^2 = 1 - x^2/vn1sq, recompute when t vn1sq/vn2sq <= tol3z.
-        double n1 = vn1[li];
-        if (n1 != 0.0) {
-          const double x = col[0];
-          double t = 1.0 - (x * x) / n1;
-          t = t < 0.0 ? 0.0 : t;
-          const double t2 = t * n1 / vn2[li];
-          if (t2 <= TOL3Z) {
-            n1 = (j + 1 < rows) ? warp_sumsq(col + 1, len - 1) : 0.0;
-            if (lane == 0) vn2[li] = n1;
-          } else {
-            n1 = n1 * t;
-          }
-          __syncwarp();
-          if (lane == 0) vn1[li] = n1;
+    {
+      const int g8 = lane >> 3, l8 = lane & 7;
+      const unsigned gmask = 0xffu << (8 * g8);
+      for (int li = warp * 4 + g8; li < nown; li += wpb * 4) {
+        const int gi = b + li * G;
+        if (gi == p || done_l[li]) continue;
+        double *col = colptr(li) + j;
+        if (tau != 0.0) {
+          double w = l8 == 0 ? col[0] : 0.0;
+          for (int r = 1 + l8; r < len; r += 8) w = fma(cp[r] * scal, col[r], w);
+          w += __shfl_xor_sync(gmask, w, 4);
+          w += __shfl_xor_sync(gmask, w, 2);
+          w += __shfl_xor_sync(gmask, w, 1);
+          w *= tau;
+          if (l8 == 0) col[0] -= w;
+          for (int r = 1 + l8; r < len; r += 8) col[r] = fma(-w, cp[r] * scal, col[r]);
+          __syncwarp(gmask);
         }
-        if (better(n1, gi, best.v, best.i)) { best.v = n1; best.i = gi; }
+        if (a.pivot) {
+          // xLAQP2 downdating on squared norms (vn1 = ||.||^2, vn2 = ||.||^2 at the last
+          // recompute): t = 1 - x^2/vn1, recompute when t vn1/vn2 <= tol3z.
+          double n1 = vn1[li];
+          if (n1 != 0.0) {
+            const double x = col[0];
+            double t = 1.0 - (x * x) / n1;
+            t = t < 0.0 ? 0.0 : t;
+            const double t2 = t * n1 / vn2[li];
+            if (t2 <= TOL3Z) {
+              double ss = 0.0;
+              for (int r = 1 + l8; r < len; r += 8) ss = fma(col[r], col[r], ss);
+              ss += __shfl_xor_sync(gmask, ss, 4);
+              ss += __shfl_xor_sync(gmask, ss, 2);
+              ss += __shfl_xor_sync(gmask, ss, 1);
+              n1 = (j + 1 < rows) ? ss : 0.0;
+              if (l8 == 0) vn2[li] = n1;
+            } else {
+              n1 = n1 * t;
+            }
+            __syncwarp(gmask);
+            if (l8 == 0) vn1[li] = n1;
+          }
+          if (better(n1, gi, best.v, best.i)) { best.v = n1; best.i = gi; }
+        }
       }
     }
     {

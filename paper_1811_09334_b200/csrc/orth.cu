@@ -205,6 +205,44 @@ __global__ void replace_dep_kernel(int64_t m, int n, double *Q, int64_t ldq, con
   }
 }
 
+// CholeskyQR2's second pass: G = Q1^T Q1 = I + E with ||E|| ~ cond(Y)^2 u.  If max|E_ij| <= 2^-27,
+// chol(I + E) = I + U with U = triu(E, 1) + diag(E)/2 + O(|E|^2) and (I + U)^-1 = I - U + O(|U|^2),
+// both exact to below u, so R and X = R^-1 come from one elementwise pass.  Otherwise sets
+// (*cond_word) |= fail_bit so the full Cholesky runs.  One CTA (n <= 1056: n^2 <= 1.2M entries).
+__global__ void __launch_bounds__(1024) near_identity_kernel(int n, const double *G, int64_t ldg, double *R,
+                                                             int64_t ldr, double *X, int64_t ldx, unsigned *cond_word,
+                                                             unsigned fail_bit, const unsigned *cond,
+                                                             unsigned cond_mask) {
+  if (cond && ((*cond) & cond_mask) == 0) return;
+  __shared__ double red[32];
+  double emax = 0.0;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    const double v = G[i + (int64_t)j * ldg] - (i == j ? 1.0 : 0.0);
+    emax = fmax(emax, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  double m = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+  if (!(m <= 0x1p-27)) {
+    if (threadIdx.x == 0) atomicOr(cond_word, fail_bit);
+    return;
+  }
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    const double g = G[i + (int64_t)j * ldg];
+    double u = 0.0;
+    if (i < j) u = g;
+    else if (i == j) u = 0.5 * (g - 1.0);
+    R[i + (int64_t)j * ldr] = (i == j ? 1.0 : 0.0) + u;
+    X[i + (int64_t)j * ldx] = (i == j ? 1.0 : 0.0) - u;
+  }
+}
+
 // G2 += s I with s = 11 (m c + c(c+1)) u tr(G2); run only if (*cond & mask).  Marks the
 // handle flag word (RQLP_FLAG_SHIFTED_CHOLQR) and the pass-3 condition bit.
 __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsigned *flag_word, unsigned *cond_word,
@@ -307,12 +345,22 @@ void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms) {
 // breakdown in the COND word.  Kernels run only if (*cond & mask) when cond given.
 static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Yin, int64_t ldyi, double *Qout,
                         int64_t ldqo, double *Rout, unsigned pass_bit, const unsigned *cond, unsigned mask,
-                        bool sharded) {
+                        bool sharded, bool second = false) {
+  const unsigned *gcond = cond;   // the pass's own condition (the GEMMs)
+  const unsigned gmask = mask;
   int64_t lc = round_up(n, 8);
   unsigned *condw = c.dflags + COND_WORD;
   const unsigned dep_bit = pass_bit << 16;
   gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask);
   if (sharded) allreduce_sum(c, s.G, lc * n);   // Gram summed over the row shards
+  if (second) {
+    // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
+    near_identity_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G, lc, Rout, lc, s.Rinv, lc, condw, pass_bit << 24,
+                                                   cond, mask);
+    RQLP_LAUNCHED(c);
+    cond = condw;
+    mask = pass_bit << 24;
+  }
   if (n > CHOL_SMALL) launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);  // blocked path destroys G
   const double *Gorig = n > CHOL_SMALL ? s.G2 : s.G;
   chol_inv(c, n, s.G, lc, Gorig, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
@@ -325,7 +373,7 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   launch_copy(c, n, n, s.G2, lc, s.G, lc, false, condw, pass_bit);
   chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
            s.partial_elems, nullptr, 0u);
-  gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, cond, mask);
+  gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, gcond, gmask);
   // rank-deficient columns -> random completion, orthonormalised by the following pass
   replace_dep_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
                            (unsigned)std::min<int64_t>(n, 64)),
@@ -346,7 +394,7 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   }
   // pass 1: Y -> Ybuf (R1 in Racc), pass 2: Ybuf -> V (R2 in R)
   cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
-  cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded);
+  cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded, true);
   if (R) {  // R = R2 R1
     gemm_generic_ex(c, false, false, n, n, n, 1.0, s.R, lc, s.Racc, lc, 0.0, s.tmp, lc, s.partials, s.partial_elems,
                     false, nullptr, 0);
@@ -355,7 +403,7 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   // pass 3 (only when pass 1 or 2 needed the shift, bits 1<<8 | 2<<8, or completed dependent
   // columns, bits 1<<16 | 2<<16): V -> Ybuf -> V
   const unsigned m3 = (1u << 8) | (2u << 8) | (1u << 16) | (2u << 16);
-  cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded);
+  cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded, true);
   launch_copy(c, m, n, s.Ybuf, s.ldy, V, ldv, false, condw, m3);
   if (R) {
     gemm_generic_ex(c, false, false, n, n, n, 1.0, s.R, lc, s.Racc, lc, 0.0, s.tmp, lc, s.partials, s.partial_elems,
