@@ -110,6 +110,23 @@ int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, 
              int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P,
              int64_t ldp, int64_t *piv0, int64_t *piv1);
 
+/* Auto-rank RQLP (the "auto-rank randomized QLP" the
+ * paper leaves as future work): the BRQLP block loop (Alg. 3, per-block sketch Y_j = AΩ_j with
+ * the first l_max columns of Ω, implicit deflation, q deflated power steps) adds blocks of b
+ * columns until the error indicator of eq. (3), ||A||_F^2 - sum_j ||B_j||_F^2,
+ * is <= (eps ||A||_F)^2 (reading R25: eps is relative to ||A||_F) or l_max columns are used.
+ * Arguments: h (1), m (2), n (3), block size b (4) >= 1, l_max (5) with b <= l_max <= min(m, n),
+ * q (6) >= 0, eps (7) >= 0, A (8) device m x n, lda (9) >= m, seed (10), Q (11) m x l_max,
+ * ldq (12), L (13) l_max x l_max, ldl (14), P (15) n x l_max, ldp (16), piv0/piv1 (17, 18)
+ * int64[l_max] (nullable), *l_out (19, host) = columns used, *err_out (20, host, nullable) =
+ * the final indicator sqrt(max(0, ||A||^2 - sum ||B_j||^2)) / ||A||_F.  The first *l_out
+ * columns of Q, P (and the leading *l_out x *l_out block of L) are the factorisation.
+ * Synchronous (one device->host read of the indicator per block). */
+int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, int q, double eps,
+                     const double *A, int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L,
+                     int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1, int *l_out,
+                     double *err_out);
+
 /* Synchronous any-pointer form of rqlp_ex / erqlp_ex / brqlp_ex on handle h: `variant` (2)
  * selects the algorithm (RQLP_VARIANT_*), d (8) is used by ERQLP, b (9) by BRQLP.  A (10), Q (13),
  * T (14), P (15) may be host (pageable or pinned) or device pointers; host operands are copied

@@ -66,6 +66,8 @@ def lib():
                                _d, _i64, _d, _i64]
         L.orc_brqlp.argtypes = [_i64, _i64, _int, _int, _int, _int, _d, _i64, _u64,
                                 _d, _i64, _d, _i64, _d, _i64, _i64p, _i64p, _d, _i64]
+        L.orc_autorank.argtypes = [_i64, _i64, _int, _int, _int, ctypes.c_double, _d, _i64, _u64, _d, _i64, _d,
+                                   _i64, _d, _i64, _i64p, _i64p, ctypes.POINTER(_int), ctypes.POINTER(ctypes.c_double)]
         L.orc_residual.argtypes = [_i64, _i64, _i64, _d, _i64, _d, _i64, _d, _i64, _d, _i64]
         L.orc_residual.restype = ctypes.c_double
         L.orc_num_threads.restype = _int
@@ -241,6 +243,26 @@ def brqlp(A, k: int, p: int, b: int, q: int = 0, seed: int = 0, stages: bool = F
     if stages:
         out.update(V=V)
     return out
+
+
+def autorank(A, b: int, l_max: int, eps: float, q: int = 0, seed: int = 0):
+    """Auto-rank RQLP (NEXT-1): blocks of b columns until ||A||^2 - sum ||B_j||^2 <= (eps ||A||)^2."""
+    A = _f(A)
+    m, n = A.shape
+    Q = np.zeros((m, l_max), order="F")
+    L = np.zeros((l_max, l_max), order="F")
+    P = np.zeros((n, l_max), order="F")
+    piv0 = np.zeros(l_max, dtype=np.int64)
+    piv1 = np.zeros(l_max, dtype=np.int64)
+    lo = ctypes.c_int(0)
+    err = ctypes.c_double(0.0)
+    rc = lib().orc_autorank(m, n, b, l_max, q, eps, _p(A), _ld(A), seed, _p(Q), _ld(Q), _p(L), _ld(L), _p(P), _ld(P),
+                            piv0.ctypes.data_as(_i64p), piv1.ctypes.data_as(_i64p), ctypes.byref(lo),
+                            ctypes.byref(err))
+    if rc != 0:
+        raise ValueError(f"orc_autorank rc={rc}")
+    l = lo.value
+    return dict(Q=Q[:, :l], T=L[:l, :l], P=P[:, :l], piv0=piv0[:l], piv1=piv1[:l], l=l, err=err.value)
 
 
 def residual(A, Q, T, P) -> float:

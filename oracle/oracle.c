@@ -617,6 +617,68 @@ int orc_brqlp(int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
   return 0;
 }
 
+int orc_autorank(int64_t m, int64_t n, int b, int l_max, int q, double eps, const double *A, int64_t lda,
+                 uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp,
+                 int64_t *piv0, int64_t *piv1, int *l_out, double *err_out) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (b < 1) return -3;
+  if (l_max < b || l_max > m || l_max > n) return -4;
+  if (q < 0) return -5;
+  if (!(eps >= 0.0)) return -6;
+  if (lda < m) return -8;
+  const int64_t l = l_max;
+  double *Aw = dalloc(m * n);
+  for (int64_t j = 0; j < n; ++j) memcpy(Aw + IDX(0, j, m), A + IDX(0, j, lda), sizeof(double) * (size_t)m);
+  const double a2 = orc_fro(m, n, A, lda) * orc_fro(m, n, A, lda);   /* ||A||_F^2 */
+  double *Om = dalloc(n * l), *Vall = dalloc(m * l);
+  orc_gaussian(seed, 0, n, l, Om, n);
+  for (int64_t i = 0; i < l; ++i)
+    for (int64_t j = 0; j < l; ++j) L[IDX(i, j, ldl)] = 0.0;
+  double b2 = 0.0;   /* sum_j ||B_j||_F^2 */
+  int64_t used = 0;
+  for (int64_t c0 = 0; c0 < l; c0 += b) {
+    const int64_t bj = (c0 + b <= l) ? b : l - c0;
+    double *Y = dalloc(m * bj), *Vj = Vall + IDX(0, c0, m), *R = dalloc(bj * bj);
+    double *Z = dalloc(n * bj), *W = dalloc(n * bj), *Bj = dalloc(bj * n);
+    orc_gemm_nn(m, bj, n, A, lda, Om + IDX(0, c0, n), n, Y, m);      /* Alg.3 l.3 (original A) */
+    orc_hqr(m, bj, Y, m, Vj, m, R, bj);
+    reorth(m, c0, bj, Vall, m, Vj);
+    for (int it = 0; it < q; ++it) {
+      orc_gemm_tn(n, bj, m, Aw, m, Vj, m, Z, n);
+      orc_hqr(n, bj, Z, n, W, n, R, bj);
+      orc_gemm_nn(m, bj, n, Aw, m, W, n, Y, m);
+      orc_hqr(m, bj, Y, m, Vj, m, R, bj);
+      reorth(m, c0, bj, Vall, m, Vj);
+    }
+    orc_gemm_tn(bj, n, m, Vj, m, Aw, m, Bj, bj);                     /* B_j = V_j^T A^(j-1) */
+#pragma omp parallel for schedule(static)
+    for (int64_t cc = 0; cc < n; ++cc)
+      for (int64_t t = 0; t < bj; ++t) {
+        double bb = Bj[IDX(t, cc, bj)];
+        double *ac = Aw + IDX(0, cc, m);
+        const double *vt = Vj + IDX(0, t, m);
+        for (int64_t i = 0; i < m; ++i) ac[i] -= vt[i] * bb;
+      }
+    const double nb = orc_fro(bj, n, Bj, bj);
+    b2 += nb * nb;
+    double *QB = dalloc(bj * bj), *Lj = dalloc(bj * bj);
+    int tu;
+    orc_qlp_tail(bj, n, Bj, bj, 0, QB, bj, Lj, bj, P + IDX(0, c0, ldp), ldp, piv0 + c0, piv1 + c0, &tu);
+    orc_gemm_nn(m, bj, bj, Vj, m, QB, bj, Q + IDX(0, c0, ldq), ldq);
+    for (int64_t j = 0; j < bj; ++j)
+      for (int64_t i = 0; i < bj; ++i) L[IDX(c0 + i, c0 + j, ldl)] = Lj[IDX(i, j, bj)];
+    free(Y); free(R); free(Z); free(W); free(Bj); free(QB); free(Lj);
+    used = c0 + bj;
+    const double e2 = a2 - b2;   /* eq. (3): ||A - P_V A||_F^2 = ||A||_F^2 - ||B||_F^2 */
+    if (err_out) *err_out = a2 > 0.0 ? sqrt(e2 > 0.0 ? e2 : 0.0) / sqrt(a2) : 0.0;
+    if (e2 <= eps * eps * a2) break;
+  }
+  *l_out = (int)used;
+  free(Aw); free(Om); free(Vall);
+  return 0;
+}
+
 double orc_residual(int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, const double *Q, int64_t ldq,
                     const double *T, int64_t ldt, const double *P, int64_t ldp) {
   double *M = dalloc(l * n); /* M = T P^T  (l x n) */

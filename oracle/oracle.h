@@ -77,6 +77,16 @@ int orc_brqlp(int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
               uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp,
               int64_t *piv0, int64_t *piv1, double *V_out, int64_t ldv);
 
+/* Auto-rank RQLP (NEXT-1; "auto-rank randomized QLP", eq. (3)):
+ * BRQLP blocks of b columns (Ω columns jb..jb+b-1 of an n x l_max Ω, explicit deflation, q
+ * deflated power steps) are added until the error indicator ||A||_F^2 - sum_j ||B_j||_F^2 <=
+ * (eps ||A||_F)^2 (reading R25) or l reaches l_max.  Returns 0; *l_out = columns used; err_out
+ * (nullable) receives the final indicator sqrt(max(0, ||A||^2 - sum ||B_j||^2)) / ||A||_F.
+ * Q (m x l_max), L (l_max x l_max), P (n x l_max): the first *l_out columns are the result. */
+int orc_autorank(int64_t m, int64_t n, int b, int l_max, int q, double eps, const double *A, int64_t lda,
+                 uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp,
+                 int64_t *piv0, int64_t *piv1, int *l_out, double *err_out);
+
 /* ||A - Q T P^T||_F computed directly, row by row (never forms m x n). */
 double orc_residual(int64_t m, int64_t n, int64_t l, const double *A, int64_t lda,
                     const double *Q, int64_t ldq, const double *T, int64_t ldt,

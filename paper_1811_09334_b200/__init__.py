@@ -342,3 +342,23 @@ def factorize_host(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 0, b: i
     _check(lib().rqlp_factorize(h.h, variant, m, n, k, p, q, d, b or 0, _ptr(A), _ld(A), seed, _ptr(Q), _ptr(T),
                                 _ptr(P), ctypes.byref(tu)), "rqlp_factorize")
     return Q, T, P, bool(tu.value)
+
+
+def autorank(A: torch.Tensor, b: int, l_max: int, eps: float, q: int = 0, seed: int = 0,
+             handle: Handle | None = None) -> dict:
+    """Auto-rank RQLP (NEXT-1): grow blocks of b columns until the eq. (3)
+    indicator sqrt(||A||^2 - sum ||B_j||^2) <= eps ||A||_F or l_max columns.  Returns the
+    factorisation restricted to the l columns used, plus l and the final indicator."""
+    A = _mat(A, "A")
+    h = _handle(handle)
+    h.clear_workspace()
+    m, n = A.shape
+    Q, L, P = cm_empty(m, l_max, A.device), cm_empty(l_max, l_max, A.device), cm_empty(n, l_max, A.device)
+    piv0 = torch.empty(l_max, dtype=torch.int64, device=A.device)
+    piv1 = torch.empty(l_max, dtype=torch.int64, device=A.device)
+    lo, err = ctypes.c_int(0), ctypes.c_double(0.0)
+    _check(lib().rqlp_autorank_ex(h.h, m, n, b, l_max, q, float(eps), _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L),
+                                  _ld(L), _ptr(P), _ld(P), _ptr(piv0), _ptr(piv1), ctypes.byref(lo),
+                                  ctypes.byref(err)), "rqlp_autorank_ex")
+    l = lo.value
+    return dict(Q=Q[:, :l], T=L[:l, :l], P=P[:, :l], piv0=piv0[:l], piv1=piv1[:l], l=l, err=err.value)

@@ -228,7 +228,8 @@ void carve_plan(Arena &a, Plan &p, int variant, int64_t m, int64_t n, int64_t l,
   tail_carve(a, p.tail, lb, n, num_sms);
   if (variant == RQLP_VARIANT_BRQLP) {
     p.C = a.take<double>(round_up(l, 8) * b);
-    p.D = a.take<double>(round_up(l, 8) * b);
+    // D holds B_<j W (c0 x b, ld ldl) and E = V_j^T V_<j (b x c0, ld round_up(b, 8))
+    p.D = a.take<double>(std::max(round_up(l, 8) * b, round_up(b, 8) * l));
     p.Qt2 = a.take<double>(p.ldm * b);
   } else {
     p.C = p.D = p.Qt2 = nullptr;
@@ -354,9 +355,17 @@ int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
 }
 
 // ---- BRQLP -------------------------------------------------------------------------------
+// Auto-rank mode of the block loop (NEXT-1): per-block sketches, and after
+// each block the eq. (3) indicator ||A||_F^2 - sum_j ||B_j||_F^2 is read back; the loop stops once
+// it is <= (eps ||A||_F)^2 (reading R25).
+struct AutoRank {
+  double eps = 0.0, a2 = 0.0, err = 0.0;
+  double *acc = nullptr, *part = nullptr;  // device: running sum_j ||B_j||^2, reduction partials
+  int l_out = 0;
+};
 void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
                    int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout,
-                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need);
+                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need, AutoRank *ar = nullptr);
 // Alg.3 with implicit deflation: A^(j-1) X = A X - V_<j (B_<j X), A^(j-1)^T V = A^T V - B_<j^T (V_<j^T V).
 int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A, int64_t lda,
               uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout, int64_t ldp, int64_t *piv0,
@@ -372,7 +381,7 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
 
 void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
                    int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *Pout,
-                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need) {
+                   int64_t ldp, int64_t *piv0, int64_t *piv1, char *ws, size_t need, AutoRank *ar) {
   const int64_t l = (int64_t)k + p;
   const bool sh = c.comm != nullptr;  // row-sharded handle: Grams are summed over ranks
   Arena a;
@@ -385,15 +394,31 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   c.mark("start");
   launch_omega(c, n, l, 0, seed, P.Om, ldn);                                            // l.1
   c.mark("omega");
-  gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);               // l.3 all Y_j = AΩ_j
-  c.mark("pass_sketch");
-  if (h->dbgY) launch_copy(c, m, l, P.Y, ldm, h->dbgY, h->ldY, false);
+  if (!ar) {
+    gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);             // l.3 all Y_j = AΩ_j
+    c.mark("pass_sketch");
+    if (h->dbgY) launch_copy(c, m, l, P.Y, ldm, h->dbgY, h->ldY, false);
+  } else {
+    // ||A||_F^2 once (one read of A), then sum_j ||B_j||^2 accumulates on the device
+    fro2_accumulate(c, m, n, A, lda, ar->part, ar->acc, true);
+    allreduce_sum(c, ar->acc, 1);  // row shards: ||A||^2 is the sum over ranks (B_j is replicated)
+    double a2 = 0.0;
+    RQLP_CUDA(cudaMemcpyAsync(&a2, ar->acc, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    RQLP_CUDA(cudaStreamSynchronize(c.stream));
+    ar->a2 = a2;
+    RQLP_CUDA(cudaMemsetAsync(ar->acc, 0, sizeof(double), c.stream));
+  }
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
   for (int64_t j = 0; j < h_blocks; ++j) {
     const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
     double *Vj = P.V + c0 * ldm;
+    if (ar) {  // Alg.3 l.3 inside the loop: Y_j = A Ω_j (original A)
+      c.mark("b_other");
+      gemm_nn(c, m, bj, n, A, lda, P.Om + c0 * ldn, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems);
+      c.mark("pass_block_sketch");
+    }
     // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
     auto reorth = [&]() {
       if (c0 == 0) return;
@@ -439,19 +464,33 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     allreduce_sum(c, Bj, ldbj * n);
     c.mark("pass_block_project");
     if (c0 > 0) {
-      gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, LL, false, P.part, P.part_elems);    // E = Vj^T V_<j (bj x c0)
-      allreduce_sum(c, P.D, LL * c0);
-      gemm_generic_ex(c, false, false, bj, n, c0, -1.0, P.D, LL, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems, false,
+      const int64_t lde = round_up(b, 8);
+      gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, lde, false, P.part, P.part_elems);   // E = Vj^T V_<j (bj x c0)
+      allreduce_sum(c, P.D, lde * c0);
+      gemm_generic_ex(c, false, false, bj, n, c0, -1.0, P.D, lde, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems, false,
                       nullptr, 0);
     }
     launch_copy(c, bj, n, Bj, ldbj, B + c0, LL, false);   // keep B_j for the later blocks' deflation
     c.mark("block_passes");
+    bool stop = false;
+    if (ar) {  // eq. (3): ||A - P_V A||_F^2 = ||A||_F^2 - sum_j ||B_j||_F^2
+      fro2_accumulate(c, bj, n, Bj, ldbj, ar->part, ar->acc, false);
+      double b2 = 0.0;
+      RQLP_CUDA(cudaMemcpyAsync(&b2, ar->acc, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+      RQLP_CUDA(cudaStreamSynchronize(c.stream));
+      const double e2 = ar->a2 - b2;
+      ar->err = ar->a2 > 0.0 ? std::sqrt(e2 > 0.0 ? e2 : 0.0) / std::sqrt(ar->a2) : 0.0;
+      ar->l_out = (int)(c0 + bj);
+      stop = e2 <= ar->eps * ar->eps * ar->a2;
+      if (getenv("RQLP_AR_DEBUG")) fprintf(stderr, "[autorank] block %lld a2 %.17g b2 %.17g\n", (long long)j, ar->a2, b2);
+    }
     // l.8: [Q_B, L_j, P_B] = qlp(B_j) (overwrites the tail's copy)
     qlp_tail(c, P.tail, bj, n, P.tail.Bw, P.tail.ldl, 0, P.QB, P.tail.ldl, L + c0 + c0 * ldl, ldl, Pout + c0 * ldp,
              ldp, piv0 ? piv0 + c0 : nullptr, piv1 ? piv1 + c0 : nullptr);
     // l.9: Q_j = V_j Q_B
     gemm_nn(c, m, bj, bj, Vj, ldm, P.QB, P.tail.ldl, Q + c0 * ldq, ldq, P.part, P.part_elems);
     c.mark("block_tail");
+    if (stop) break;
   }
   if (h->dbgV) launch_copy(c, m, l, P.V, ldm, h->dbgV, h->ldV, false);
   if (h->dbgB) launch_copy(c, l, n, B, LL, h->dbgB, h->ldB, false);
@@ -639,6 +678,44 @@ int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, 
   if (ldp < n) return -16;
   return guarded(h, [&] {
     return run_brqlp(h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
+  });
+}
+
+int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, int q, double eps, const double *A,
+                     int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P,
+                     int64_t ldp, int64_t *piv0, int64_t *piv1, int *l_out, double *err_out) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 1) return -2;
+  if (n < 1) return -3;
+  if (b < 1) return -4;
+  if (l_max < b || l_max > n || (h->nranks == 1 && l_max > m)) return -5;
+  if (q < 0) return -6;
+  if (!(eps >= 0.0)) return -7;
+  if (!A) return -8;
+  if (lda < m) return -9;
+  if (!Q) return -11;
+  if (ldq < m) return -12;
+  if (!L) return -13;
+  if (ldl < l_max) return -14;
+  if (!P) return -15;
+  if (ldp < n) return -16;
+  if (!l_out) return -19;
+  return guarded(h, [&] {
+    const size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l_max, b, h->num_sms);
+    char *ws = get_ws(h, need + 1032 * 8 + 256, true);
+    AutoRank ar;
+    ar.eps = eps;
+    ar.acc = reinterpret_cast<double *>(ws + ((need + 255) & ~(size_t)255));
+    ar.part = ar.acc + 8;
+    Ctx c = make_ctx(h);
+    reset_timing(h);
+    // k + p = l_max for the plan; the loop stops at the first block meeting the tolerance
+    enqueue_brqlp(c, h, m, n, l_max - 1, 1, b, q, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, ws, need, &ar);
+    h->launches = c.launches;
+    RQLP_CUDA(cudaStreamSynchronize(c.stream));
+    *l_out = ar.l_out;
+    if (err_out) *err_out = ar.err;
+    return RQLP_OK;
   });
 }
 

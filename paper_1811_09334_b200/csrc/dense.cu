@@ -105,3 +105,48 @@ void residual_sq(Ctx &c, int64_t m, int64_t n, int64_t l, const double *A, int64
 }
 
 }  // namespace rqlpk
+
+namespace rqlpk {
+namespace {
+
+// part[b] = sum of squares of the columns b, b + gridDim.x, ... of X (rows x cols, ld), fixed order.
+__global__ void colsumsq_kernel(int64_t rows, int64_t cols, const double *__restrict__ X, int64_t ldx,
+                                double *part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t j = blockIdx.x; j < cols; j += gridDim.x) {
+    const double *x = X + j * ldx;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) s = fma(x[i], x[i], s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void accumulate_parts_kernel(int nparts, const double *part, double *out, int first) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = first ? 0.0 : *out;
+    for (int i = 0; i < nparts; ++i) t += part[i];
+    *out = t;
+  }
+}
+
+}  // namespace
+
+// *out (+)= ||X||_F^2 (X rows x cols, ld), deterministic fixed-order reduction; part >= 1024 doubles.
+void fro2_accumulate(Ctx &c, int64_t rows, int64_t cols, const double *X, int64_t ldx, double *part, double *out,
+                     bool first) {
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cols, 1024));
+  colsumsq_kernel<<<nb, 256, 0, c.stream>>>(rows, cols, X, ldx, part);
+  RQLP_LAUNCHED(c);
+  accumulate_parts_kernel<<<1, 32, 0, c.stream>>>(nb, part, out, first ? 1 : 0);
+  RQLP_LAUNCHED(c);
+}
+
+}  // namespace rqlpk

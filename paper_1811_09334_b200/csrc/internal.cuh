@@ -28,10 +28,18 @@ struct CudaError : std::runtime_error {
                               __FILE__ + ":" + std::to_string(__LINE__));                      \
   } while (0)
 
+// RQLP_SYNC_DEBUG=1: synchronise after every eager launch so a faulting kernel is named.
+static inline bool sync_debug() {
+  static const bool on = getenv("RQLP_SYNC_DEBUG") != nullptr;
+  return on;
+}
+
 #define RQLP_LAUNCHED(ctx)                                                                     \
   do {                                                                                         \
     (ctx).launches++;                                                                          \
     cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ == cudaSuccess && ::rqlpk::sync_debug() && !(ctx).capturing)                               \
+      e_ = cudaStreamSynchronize((ctx).stream);                                                \
     if (e_ != cudaSuccess)                                                                     \
       throw ::rqlpk::CudaError(std::string("launch: ") + cudaGetErrorString(e_) + " @" +        \
                               __FILE__ + ":" + std::to_string(__LINE__));                      \
@@ -164,6 +172,10 @@ void tail_carve(Arena &a, TailScratch &s, int64_t l, int64_t n, int num_sms);
 // B (l x n) is overwritten.  Outputs QB (l x l), T, PB (n x l), piv0/piv1 (device int64, nullable).
 void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t ldb, int d, double *QB,
               int64_t ldqb, double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1);
+
+// *out (+)= ||X||_F^2, deterministic (dense.cu); part >= 1024 doubles
+void fro2_accumulate(Ctx &c, int64_t rows, int64_t cols, const double *X, int64_t ldx, double *part, double *out,
+                     bool first);
 
 // ---- residual (dense.cu) ----
 void residual_sq(Ctx &c, int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, const double *Q,

@@ -277,3 +277,34 @@ def test_deterministic_reruns(rq):
     b = rq.factorize(A, 100, 10, q=1, d=2, seed=2)
     for key in ("Q", "T", "P", "piv0"):
         assert torch.equal(a[key], b[key])
+
+
+# ------------------------------------------------------------------ NEXT-1: auto-rank RQLP
+@pytest.mark.parametrize("m,n,b,l_max,eps,q", [(1500, 700, 16, 256, 1e-2, 1), (1200, 900, 24, 100, 0.0, 0),
+                                               (900, 600, 32, 320, 1e-3, 2), (400, 300, 8, 64, 1.0, 0)])
+def test_autorank_parity(rq, orc, m, n, b, l_max, eps, q):
+    """Auto-rank RQLP (eq. (3) indicator): same stopping block, pivots and
+    L-values as the oracle; the reported indicator equals the direct residual.  (1200, 900, 24, 100,
+    eps=0) runs to l_max with a ragged last block; eps = 1 stops after the first block."""
+    sig = np.exp(-np.arange(1, min(m, n) + 1.0) / 40)
+    A = _rand_svd(m, n, sig, m + 3 * n)
+    g = rq.autorank(_cm(A), b=b, l_max=l_max, eps=eps, q=q, seed=6)
+    o = orc.autorank(A, b=b, l_max=l_max, eps=eps, q=q, seed=6)
+    assert g["l"] == o["l"], (g["l"], o["l"])
+    l = g["l"]
+    _check_factorization(rq, orc, A, g, o, l)
+    assert g["err"] == pytest.approx(o["err"], rel=1e-8, abs=1e-13)
+    direct = orc.residual(A, _np(g["Q"]), _np(g["T"]), _np(g["P"])) / np.linalg.norm(A)
+    assert g["err"] == pytest.approx(direct, rel=1e-6, abs=1e-13)
+    if eps > 0 and l < l_max:
+        assert g["err"] <= eps
+
+
+def test_autorank_argument_errors(rq):
+    A = torch.zeros(10, 8, dtype=torch.float64, device="cuda").t().contiguous().t()
+    with pytest.raises(rq.RQLPError):
+        rq.autorank(A, b=4, l_max=2, eps=0.1)     # l_max < b
+    with pytest.raises(rq.RQLPError):
+        rq.autorank(A, b=2, l_max=9, eps=0.1)     # l_max > n
+    with pytest.raises(rq.RQLPError):
+        rq.autorank(A, b=2, l_max=4, eps=-1.0)    # eps < 0

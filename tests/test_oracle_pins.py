@@ -368,3 +368,54 @@ def test_zero_matrix(orc):
 def test_sigma_helpers():
     s = sigma("poly2", 4).numpy()
     np.testing.assert_allclose(s, [1, 1 / 4, 1 / 9, 1 / 16])
+
+
+# ------------------------------------------------------------------ NEXT-1: auto-rank RQLP
+def test_autorank_indicator_is_direct_residual(orc):
+    """The eq. (3) indicator, computed from ||A||^2 - sum ||B_j||^2, equals the
+    directly computed ||A − QLPᵀ||_F / ||A||_F at every stopping point (catches a missing deflation
+    of B_j, a wrong block offset, or an indicator on the wrong matrix)."""
+    sig = np.exp(-np.arange(1, 151.0) / 15)
+    A = _rand_svd(220, 150, sig, 41)
+    nA = np.linalg.norm(A)
+    prev = 0
+    for eps in (1e-1, 1e-2, 1e-3):
+        out = orc.autorank(A, b=8, l_max=144, eps=eps, q=1, seed=3)
+        direct = orc.residual(A, out["Q"], out["T"], out["P"]) / nA
+        assert out["err"] == pytest.approx(direct, rel=1e-6, abs=1e-13)
+        assert out["err"] <= eps and out["l"] % 8 == 0 and out["l"] >= prev
+        # one block fewer would not have met the tolerance (stops at the FIRST block)
+        if out["l"] > 8:
+            o2 = orc.autorank(A, b=8, l_max=out["l"] - 8, eps=0.0, q=1, seed=3)
+            assert orc.residual(A, o2["Q"], o2["T"], o2["P"]) / nA > eps
+        prev = out["l"]
+
+
+def test_autorank_exact_rank(orc):
+    """rank(A) = 24 = 3 blocks of 8: the indicator collapses to rounding at l = 24 and the loop
+    stops there (a textbook property of the range finder on an exactly low-rank matrix)."""
+    sig = np.linspace(4.0, 1.0, 24)
+    A = _rand_svd(200, 140, sig, 42)
+    out = orc.autorank(A, b=8, l_max=80, eps=1e-10, q=0, seed=5)
+    assert out["l"] == 24
+    assert out["err"] < 1e-12
+    Q = out["Q"]
+    assert np.abs(Q.T @ Q - np.eye(24)).max() < 1e-13 * 24
+    np.testing.assert_allclose(Q @ out["T"] @ out["P"].T, A, atol=1e-12 * np.linalg.norm(A))
+
+
+def test_autorank_limits_and_equivalence(orc):
+    """eps >= 1 stops after one block; eps = 0 runs to l_max; the result at l_out is the
+    BRQLP of Alg. 3 with k + p = l_out on the same Ω (Ω columns do not depend on l)."""
+    sig = np.arange(1, 121.0) ** -1.5
+    A = _rand_svd(180, 120, sig, 43)
+    one = orc.autorank(A, b=10, l_max=60, eps=1.0, q=0, seed=8)
+    assert one["l"] == 10
+    full = orc.autorank(A, b=10, l_max=60, eps=0.0, q=0, seed=8)
+    assert full["l"] == 60
+    mid = orc.autorank(A, b=10, l_max=60, eps=3e-2, q=1, seed=8)
+    assert 10 < mid["l"] < 60
+    ref = orc.brqlp(A, k=mid["l"] - 2, p=2, b=10, q=1, seed=8)
+    for key in ("Q", "T", "P"):
+        np.testing.assert_allclose(mid[key], ref[key], atol=1e-13)
+    assert np.array_equal(mid["piv0"], ref["piv0"]) and np.array_equal(mid["piv1"], ref["piv1"])
