@@ -38,6 +38,7 @@ extern "C" {
 #define RQLP_ERR_INTERNAL 4
 #define RQLP_ERR_DEVICE 5        /* device is not sm_100 (B200) */
 #define RQLP_ERR_HANDLE 6        /* NULL / destroyed handle */
+#define RQLP_ERR_UNSUPPORTED 7   /* operation not available on this handle (e.g. distributed) */
 
 #define RQLP_VARIANT_RQLP 0      /* Algorithm 1 */
 #define RQLP_VARIANT_ERQLP 1     /* Algorithm 2 */
@@ -109,6 +110,20 @@ int erqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
 int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
              int64_t lda, uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P,
              int64_t ldp, int64_t *piv0, int64_t *piv1);
+
+/* Truncated pivoted QLP: the deterministic rank-l QLP the paper compares
+ * against (Stewart's pivoted QLP, truncated as in PAPER.md:177-179): partial
+ * CPQR A Π0(:, 1:l) = Q_R [R11 R12] (l Householder steps, same pivot rule as the RQLP tail,
+ * reading R5), then the full CPQR [R11 R12]^T Π1 = P^ L^T; Q = Q_R Π1, P = Π0 P^.
+ * Arguments: h (1), m (2), n (3), l (4) with 1 <= l <= min(m, n), A (5) device m x n
+ * column-major, read only, lda (6) >= m, Q (7) device m x l, ldq (8) >= m, L (9) device l x l
+ * lower triangular, ldl (10) >= l, P (11) device n x l, ldp (12) >= n, piv0 / piv1 (13, 14)
+ * device int64[l] (nullable): Π0's first l columns (original indices) and Π1.  Asynchronous on
+ * the handle's stream; workspace: the caller's (if set and large enough) or library-owned.
+ * Not available on distributed handles (RQLP_ERR_UNSUPPORTED). */
+int rqlp_tqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int l, const double *A, int64_t lda, double *Q,
+                 int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp, int64_t *piv0,
+                 int64_t *piv1);
 
 /* Auto-rank RQLP (the "auto-rank randomized QLP" the
  * paper leaves as future work): the BRQLP block loop (Alg. 3, per-block sketch Y_j = AΩ_j with

@@ -58,6 +58,8 @@ def lib():
         L.orc_fro.restype = ctypes.c_double
         L.orc_hqr.argtypes = [_i64, _i64, _d, _i64, _d, _i64, _d, _i64]
         L.orc_cpqr.argtypes = [_i64, _i64, _d, _i64, _d, _i64, _d, _i64, _i64p]
+        L.orc_cpqr_partial.argtypes = [_i64, _i64, _i64, _d, _i64, _d, _i64, _d, _i64, _i64p]
+        L.orc_tqlp.argtypes = [_i64, _i64, _i64, _d, _i64, _d, _i64, _d, _i64, _d, _i64, _i64p, _i64p]
         L.orc_svd_values.argtypes = [_i64, _i64, _d, _i64, _d]
         L.orc_qlp_tail.argtypes = [_i64, _i64, _d, _i64, _int, _d, _i64, _d, _i64, _d, _i64,
                                    _i64p, _i64p, ctypes.POINTER(_int)]
@@ -168,6 +170,35 @@ def cpqr(A):
     if rc != 0:
         raise ValueError(f"orc_cpqr rc={rc}")
     return Q, R, perm
+
+
+def cpqr_partial(A, k: int):
+    """First k steps of the pivoted Householder QR: Q (m x k), R (k x n, pivot order), perm."""
+    A = _f(A)
+    m, n = A.shape
+    Q = np.zeros((m, k), order="F")
+    R = np.zeros((k, n), order="F")
+    perm = np.zeros(n, dtype=np.int64)
+    rc = lib().orc_cpqr_partial(m, n, k, _p(A), _ld(A), _p(Q), _ld(Q), _p(R), _ld(R), perm.ctypes.data_as(_i64p))
+    if rc != 0:
+        raise ValueError(f"orc_cpqr_partial rc={rc}")
+    return Q, R, perm
+
+
+def tqlp(A, l: int):
+    """Truncated pivoted QLP (NEXT-3): dict(Q, T, P, piv0, piv1)."""
+    A = _f(A)
+    m, n = A.shape
+    Q = np.zeros((m, l), order="F")
+    L = np.zeros((l, l), order="F")
+    P = np.zeros((n, l), order="F")
+    piv0 = np.zeros(l, dtype=np.int64)
+    piv1 = np.zeros(l, dtype=np.int64)
+    rc = lib().orc_tqlp(m, n, l, _p(A), _ld(A), _p(Q), _ld(Q), _p(L), _ld(L), _p(P), _ld(P),
+                        piv0.ctypes.data_as(_i64p), piv1.ctypes.data_as(_i64p))
+    if rc != 0:
+        raise ValueError(f"orc_tqlp rc={rc}")
+    return dict(Q=Q, T=L, P=P, piv0=piv0, piv1=piv1)
 
 
 def svd_values(A):

@@ -263,8 +263,10 @@ static void form_q(int64_t m, int64_t s, const double *W, int64_t ldw, const dou
  * Pivoting (reading R5): at step j choose the remaining column with the
  * largest downdated norm, ties -> lowest ORIGINAL column index; swap; reflect; downdate the
  * norms with the xLAQP2 rule (tol3z = sqrt(2^-53)). */
-static void qr_core(int64_t m, int64_t n, double *W, int64_t ldw, double *tau, int64_t *perm, int pivot) {
+static void qr_core(int64_t m, int64_t n, double *W, int64_t ldw, double *tau, int64_t *perm, int pivot,
+                    int64_t steps) {
   int64_t s = m < n ? m : n;
+  if (steps >= 0 && steps < s) s = steps; /* partial (truncated) factorisation */
   for (int64_t i = 0; i < n; ++i) perm[i] = i;
   double *vn1 = NULL, *vn2 = NULL;
   const double tol3z = sqrt(0x1p-53);
@@ -330,9 +332,8 @@ static void qr_core(int64_t m, int64_t n, double *W, int64_t ldw, double *tau, i
 }
 
 /* Extract R (s x n upper trapezoidal) and explicit Q (m x s), then normalise R_ii >= 0. */
-static void qr_outputs(int64_t m, int64_t n, const double *W, int64_t ldw, const double *tau, double *Q,
-                       int64_t ldq, double *R, int64_t ldr) {
-  int64_t s = m < n ? m : n;
+static void qr_outputs(int64_t m, int64_t n, int64_t s, const double *W, int64_t ldw, const double *tau,
+                       double *Q, int64_t ldq, double *R, int64_t ldr) {
   if (Q) form_q(m, s, W, ldw, tau, Q, ldq);
   if (R)
     for (int64_t j = 0; j < n; ++j)
@@ -356,8 +357,8 @@ int orc_hqr(int64_t m, int64_t n, const double *A, int64_t lda, double *Q, int64
   double *tau = (double *)malloc(sizeof(double) * (size_t)(n + 1));
   int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
   for (int64_t j = 0; j < n; ++j) memcpy(W + IDX(0, j, m), A + IDX(0, j, lda), sizeof(double) * (size_t)m);
-  qr_core(m, n, W, m, tau, perm, 0);
-  qr_outputs(m, n, W, m, tau, Q, ldq, R, ldr);
+  qr_core(m, n, W, m, tau, perm, 0, -1);
+  qr_outputs(m, n, n, W, m, tau, Q, ldq, R, ldr);
   free(W); free(tau); free(perm);
   return 0;
 }
@@ -371,8 +372,24 @@ int orc_cpqr(int64_t m, int64_t n, const double *A, int64_t lda, double *Q, int6
   double *W = (double *)malloc(sizeof(double) * (size_t)(m * n + 1));
   double *tau = (double *)malloc(sizeof(double) * (size_t)(s + 1));
   for (int64_t j = 0; j < n; ++j) memcpy(W + IDX(0, j, m), A + IDX(0, j, lda), sizeof(double) * (size_t)m);
-  qr_core(m, n, W, m, tau, perm, 1);
-  qr_outputs(m, n, W, m, tau, Q, ldq, R, ldr);
+  qr_core(m, n, W, m, tau, perm, 1, -1);
+  qr_outputs(m, n, s, W, m, tau, Q, ldq, R, ldr);
+  free(W); free(tau);
+  return 0;
+}
+
+int orc_cpqr_partial(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, double *Q, int64_t ldq,
+                     double *R, int64_t ldr, int64_t *perm) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  int64_t s = m < n ? m : n;
+  if (k < 0 || k > s) return -3;
+  if (lda < (m > 1 ? m : 1)) return -5;
+  double *W = (double *)malloc(sizeof(double) * (size_t)(m * n + 1));
+  double *tau = (double *)malloc(sizeof(double) * (size_t)(k + 1));
+  for (int64_t j = 0; j < n; ++j) memcpy(W + IDX(0, j, m), A + IDX(0, j, lda), sizeof(double) * (size_t)m);
+  qr_core(m, n, W, m, tau, perm, 1, k);
+  qr_outputs(m, n, k, W, m, tau, Q, ldq, R, ldr);
   free(W); free(tau);
   return 0;
 }
@@ -676,6 +693,34 @@ int orc_autorank(int64_t m, int64_t n, int b, int l_max, int q, double eps, cons
   }
   *l_out = (int)used;
   free(Aw); free(Om); free(Vall);
+  return 0;
+}
+
+/* Truncated pivoted QLP (NEXT-3): Stewart's pivoted QLP truncated to rank l
+ * as the paper describes it: "apply partial CPQR decomposition on the m-by-n
+ * matrix A, i.e. A Π(:, 1:l) = Q R, and compute the full CPQR decomposition of the n-by-l matrix
+ * [R11 R12]^T".  With [R11 R12]^T Π1 = P^ L^T: Q = Q_R Π1, L, P = Π0 P^ (eq. (1)). */
+int orc_tqlp(int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, double *Q, int64_t ldq, double *L,
+             int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (l < 1 || l > m || l > n) return -3;
+  if (lda < m) return -5;
+  double *QR = dalloc(m * l), *R = dalloc(l * n), *Rt = dalloc(n * l), *Ph = dalloc(n * l), *Lt = dalloc(l * l);
+  int64_t *perm0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t *perm1 = (int64_t *)malloc(sizeof(int64_t) * (size_t)l);
+  orc_cpqr_partial(m, n, l, A, lda, QR, m, R, l, perm0);   /* A Π0(:, 1:l) = Q_R [R11 R12] */
+  transpose(l, n, R, l, Rt, n);                              /* [R11 R12]^T, n x l */
+  orc_cpqr(n, l, Rt, n, Ph, n, Lt, l, perm1);               /* [R11 R12]^T Π1 = P^ L^T */
+  transpose(l, l, Lt, l, L, ldl);
+  for (int64_t t = 0; t < l; ++t) {
+    piv0[t] = perm0[t];
+    piv1[t] = perm1[t];
+    for (int64_t i = 0; i < m; ++i) Q[IDX(i, t, ldq)] = QR[IDX(i, perm1[t], m)];   /* Q = Q_R Π1 */
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t t = 0; t < l; ++t) P[IDX(perm0[i], t, ldp)] = Ph[IDX(i, t, n)];    /* P = Π0 P^ */
+  free(QR); free(R); free(Rt); free(Ph); free(Lt); free(perm0); free(perm1);
   return 0;
 }
 

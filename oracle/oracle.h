@@ -52,6 +52,10 @@ int orc_hqr(int64_t m, int64_t n, const double *A, int64_t lda, double *Q, int64
 int orc_cpqr(int64_t m, int64_t n, const double *A, int64_t lda, double *Q, int64_t ldq,
              double *R, int64_t ldr, int64_t *perm);
 
+/* Partial CPQR: the first k (<= min(m,n)) steps of orc_cpqr.  Q m x k, R k x n (pivot order). */
+int orc_cpqr_partial(int64_t m, int64_t n, int64_t k, const double *A, int64_t lda, double *Q, int64_t ldq,
+                     double *R, int64_t ldr, int64_t *perm);
+
 /* One-sided Jacobi SVD (Hestenes): all min(m,n) singular values, descending. */
 int orc_svd_values(int64_t m, int64_t n, const double *A, int64_t lda, double *s);
 
@@ -86,6 +90,11 @@ int orc_brqlp(int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
 int orc_autorank(int64_t m, int64_t n, int b, int l_max, int q, double eps, const double *A, int64_t lda,
                  uint64_t seed, double *Q, int64_t ldq, double *L, int64_t ldl, double *P, int64_t ldp,
                  int64_t *piv0, int64_t *piv1, int *l_out, double *err_out);
+
+/* Truncated pivoted QLP (NEXT-3): partial CPQR of A (l steps), then
+ * CPQR of [R11 R12]^T.  Q m x l, L l x l lower, P n x l, piv0/piv1 int64[l]. */
+int orc_tqlp(int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, double *Q, int64_t ldq, double *L,
+             int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1);
 
 /* ||A - Q T P^T||_F computed directly, row by row (never forms m x n). */
 double orc_residual(int64_t m, int64_t n, int64_t l, const double *A, int64_t lda,

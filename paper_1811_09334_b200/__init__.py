@@ -362,3 +362,18 @@ def autorank(A: torch.Tensor, b: int, l_max: int, eps: float, q: int = 0, seed: 
                                   ctypes.byref(err)), "rqlp_autorank_ex")
     l = lo.value
     return dict(Q=Q[:, :l], T=L[:l, :l], P=P[:, :l], piv0=piv0[:l], piv1=piv1[:l], l=l, err=err.value)
+
+
+def tqlp(A: torch.Tensor, l: int, handle: Handle | None = None) -> dict:
+    """Truncated pivoted QLP (NEXT-3): partial CPQR of A (l steps)
+    then the CPQR of [R11 R12]^T.  Returns Q (m x l), T = L (l x l lower), P (n x l), piv0, piv1."""
+    A = _mat(A, "A")
+    h = _handle(handle)
+    h.clear_workspace()
+    m, n = A.shape
+    Q, L, P = cm_empty(m, l, A.device), cm_empty(l, l, A.device), cm_empty(n, l, A.device)
+    piv0 = torch.empty(l, dtype=torch.int64, device=A.device)
+    piv1 = torch.empty(l, dtype=torch.int64, device=A.device)
+    _check(lib().rqlp_tqlp_ex(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
+                              _ptr(piv0), _ptr(piv1)), "rqlp_tqlp_ex")
+    return dict(Q=Q, T=L, P=P, piv0=piv0, piv1=piv1, t_is_upper=False)

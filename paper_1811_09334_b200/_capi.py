@@ -28,6 +28,7 @@ SIGNATURES = [
                         ctypes.POINTER(_int), _vp, _i64, _vp]),
     ("brqlp_ex", _int, [_vp, _i64, _i64, _int, _int, _int, _int, _vp, _i64, _u64, _vp, _i64, _vp, _i64, _vp, _i64,
                         _vp, _vp]),
+    ("rqlp_tqlp_ex", _int, [_vp, _i64, _i64, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     ("rqlp_autorank_ex", _int, [_vp, _i64, _i64, _int, _int, _int, ctypes.c_double, _vp, _i64, _u64, _vp, _i64,
                                 _vp, _i64, _vp, _i64, _vp, _vp, ctypes.POINTER(_int), ctypes.POINTER(ctypes.c_double)]),
     ("rqlp_factorize", _int, [_vp, _int, _i64, _i64, _int, _int, _int, _int, _int, _vp, _i64, _u64, _vp, _vp, _vp,

@@ -497,6 +497,48 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
 }
 
 }  // namespace
+// ---- truncated pivoted QLP (NEXT-3) ---------------------------------------------------------
+struct TqlpPlan {
+  int64_t ldm;
+  double *W, *QR;
+  HHScratch hA;
+  TailScratch tail;
+};
+
+void carve_tqlp(Arena &a, TqlpPlan &p, int64_t m, int64_t n, int64_t l, int num_sms) {
+  p.ldm = round_up(m, 8);
+  p.W = a.take<double>(p.ldm * n);
+  p.QR = a.take<double>(p.ldm * l);
+  hh_carve(a, p.hA, m, n, num_sms, l);
+  tail_carve(a, p.tail, l, n, num_sms);
+}
+
+size_t tqlp_bytes(int64_t m, int64_t n, int64_t l, int num_sms) {
+  Arena a;
+  TqlpPlan p;
+  carve_tqlp(a, p, m, n, l, num_sms);
+  return a.used + 4096;
+}
+
+int run_tqlp(rqlp_handle_t h, int64_t m, int64_t n, int64_t l, const double *A, int64_t lda, double *Q, int64_t ldq,
+             double *L, int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1) {
+  const size_t need = tqlp_bytes(m, n, l, h->num_sms);
+  char *ws = get_ws(h, need, true);
+  const std::string key = make_key(h, "tqlp", {m, n, l, lda, ldq, ldl, ldp}, {A, Q, L, P, piv0, piv1, ws});
+  return with_graph(h, key, [&](Ctx &c) {
+    Arena a;
+    a.base = ws;
+    a.cap = need;
+    TqlpPlan p;
+    carve_tqlp(a, p, m, n, l, c.num_sms);
+    RQLP_CUDA(cudaMemsetAsync(c.dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned), c.stream));
+    c.mark("start");
+    launch_copy(c, m, n, A, lda, p.W, p.ldm, false);   // the engine factors in place
+    c.mark("tqlp_copy");
+    tqlp(c, p.tail, p.hA, m, n, l, p.W, p.ldm, Q, ldq, L, ldl, P, ldp, piv0, piv1, p.QR, p.ldm);
+  });
+}
+
 }  // namespace rqlpk
 
 using namespace rqlpk;
@@ -679,6 +721,24 @@ int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, 
   return guarded(h, [&] {
     return run_brqlp(h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
   });
+}
+
+int rqlp_tqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int l, const double *A, int64_t lda, double *Q, int64_t ldq,
+                 double *L, int64_t ldl, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  if (m < 1) return -2;
+  if (n < 1) return -3;
+  if (l < 1 || l > m || l > n) return -4;
+  if (!A) return -5;
+  if (lda < m) return -6;
+  if (!Q) return -7;
+  if (ldq < m) return -8;
+  if (!L) return -9;
+  if (ldl < l) return -10;
+  if (!P) return -11;
+  if (ldp < n) return -12;
+  if (h->comm) return RQLP_ERR_UNSUPPORTED;
+  return guarded(h, [&] { return run_tqlp(h, m, n, l, A, lda, Q, ldq, L, ldl, P, ldp, piv0, piv1); });
 }
 
 int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, int q, double eps, const double *A,

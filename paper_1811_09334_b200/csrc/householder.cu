@@ -386,13 +386,14 @@ __global__ void extract_r_kernel(int steps, int cols, const double *M, int64_t l
 
 // Explicit Q(:, t) = H_0 .. H_t e_t (xORG2R), one warp per column kept in shared memory, then
 // signed by sign(beta_t).  The reflectors are staged in shared memory when they fit.
-template <bool VSMEM>
+// QSMEM false (very tall Q): the column is accumulated in place in Q itself.
+template <bool VSMEM, bool QSMEM>
 __global__ void form_q_kernel(int rows, int steps, const double *Vst, const double *tau, const double *beta,
                               double *Q, int64_t ldq) {
   extern __shared__ double fsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double *vs = fsm;
-  double *q = fsm + (VSMEM ? (int64_t)rows * steps : 0) + (int64_t)warp * rows;
+  double *qs = fsm + (VSMEM ? (int64_t)rows * steps : 0) + (int64_t)warp * rows;
   __shared__ double taus[1056];
   const int tmax = min(steps, (int)((blockIdx.x + 1) * nw * 1));  // unused guard
   (void)tmax;
@@ -403,6 +404,8 @@ __global__ void form_q_kernel(int rows, int steps, const double *Vst, const doub
   const double *V = VSMEM ? vs : Vst;
   const int W = gridDim.x * nw;
   for (int t = blockIdx.x * nw + warp; t < steps; t += W) {
+    double *out = Q + (int64_t)t * ldq;
+    double *q = QSMEM ? qs : out;
     for (int r = lane; r < rows; r += 32) q[r] = (r == t) ? 1.0 : 0.0;
     __syncwarp();
     for (int j = t; j >= 0; --j) {
@@ -416,7 +419,6 @@ __global__ void form_q_kernel(int rows, int steps, const double *Vst, const doub
       __syncwarp();
     }
     const double sg = beta[t] < 0.0 ? -1.0 : 1.0;
-    double *out = Q + (int64_t)t * ldq;
     for (int r = lane; r < rows; r += 32) out[r] = sg * q[r];
     __syncwarp();
   }
@@ -429,8 +431,9 @@ __global__ void copy_perm_kernel(int64_t count, const int64_t *src, int64_t *dst
 
 }  // namespace
 
-void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms) {
-  int64_t steps = std::min(rows, cols);
+void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms, int64_t steps) {
+  steps = steps < 0 ? std::min(rows, cols) : std::min(steps, std::min(rows, cols));
+  s.max_steps = steps;
   s.max_rows = rows;
   s.max_cols = cols;
   s.max_slots = num_sms;
@@ -453,12 +456,14 @@ static void set_engine_attr() {
   }
 }
 
-void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot) {
-  if (rows > s.max_rows || cols > s.max_cols) throw std::runtime_error("hh_factor: scratch too small");
+void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot, int64_t steps) {
+  steps = steps < 0 ? std::min(rows, cols) : std::min(steps, std::min(rows, cols));
+  if (rows > s.max_rows || cols > s.max_cols || steps > s.max_steps)
+    throw std::runtime_error("hh_factor: scratch too small");
   constexpr size_t SMEM_MAX = 220 * 1024;
   EngineArgs a;
   a.M = M; a.ldm = ldm; a.rows = (int)rows; a.cols = (int)cols;
-  a.steps = (int)std::min(rows, cols); a.pivot = pivot ? 1 : 0;
+  a.steps = (int)steps; a.pivot = pivot ? 1 : 0;
   a.Vst = s.Vst; a.tau = s.tau; a.beta = s.beta; a.rec = s.rec; a.cand = s.cand; a.done = s.done; a.perm = s.perm;
   a.epoch = 0;
   a.trace = c.trace;
@@ -512,8 +517,8 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
 }
 
 void hh_extract_r(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, const double *M, int64_t ldm, double *R,
-                  int64_t ldr, bool transpose) {
-  int64_t steps = std::min(rows, cols);
+                  int64_t ldr, bool transpose, int64_t steps) {
+  steps = steps < 0 ? std::min(rows, cols) : std::min(steps, std::min(rows, cols));
   int64_t total = steps * cols;
   int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)c.num_sms * 8);
   extract_r_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>((int)steps, (int)cols, M, ldm, s.beta, s.perm, R, ldr,
@@ -521,23 +526,31 @@ void hh_extract_r(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, const double
   RQLP_LAUNCHED(c);
 }
 
-void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq) {
-  int64_t steps = std::min(rows, cols);
+void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq, int64_t steps) {
+  steps = steps < 0 ? std::min(rows, cols) : std::min(steps, std::min(rows, cols));
   if (steps > 1056) throw std::runtime_error("hh_form_q: more than 1056 reflectors");
-  const int nw = 8;
-  const size_t vbytes = (size_t)rows * steps * 8, qbytes = (size_t)nw * rows * 8;
+  const size_t vbytes = (size_t)rows * steps * 8;
+  // warps per CTA: 8, fewer when a column per warp does not fit in 200 KB (tall Q), and the
+  // column lives in Q itself beyond that
+  int nw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / ((int64_t)rows * 8)));
+  const bool qsmem = (size_t)rows * 8 <= 200 * 1024;
+  if (!qsmem) nw = 8;
+  const size_t qbytes = qsmem ? (size_t)nw * rows * 8 : 0;
   static bool attr = false;
   if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(steps, nw), (int64_t)c.num_sms));
-  if (vbytes + qbytes <= 190 * 1024) {
-    form_q_kernel<true><<<grid, nw * 32, vbytes + qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q,
-                                                                     ldq);
+  if (qsmem && vbytes + qbytes <= 190 * 1024) {
+    form_q_kernel<true, true><<<grid, nw * 32, vbytes + qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau,
+                                                                           s.beta, Q, ldq);
+  } else if (qsmem) {
+    form_q_kernel<false, true><<<grid, nw * 32, qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q,
+                                                                    ldq);
   } else {
-    form_q_kernel<false><<<grid, nw * 32, qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q, ldq);
+    form_q_kernel<false, false><<<grid, nw * 32, 0, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau, s.beta, Q, ldq);
   }
   RQLP_LAUNCHED(c);
 }

@@ -146,18 +146,20 @@ struct HHScratch {
   unsigned long long *rec = nullptr, *cand = nullptr;
   int *done = nullptr;
   int64_t *perm = nullptr;
-  int64_t max_rows = 0, max_cols = 0, max_slots = 0;
+  int64_t max_rows = 0, max_cols = 0, max_slots = 0, max_steps = 0;
 };
-void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms);
-// In-place Householder QR (pivot: column-pivoted, Golub + LAPACK downdating) of M.
-// Outputs in s: Vst, tau, beta, perm (full permutation).  M keeps R entries above the diagonal
-// of each step's pivot column in ORIGINAL column positions.
-void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot);
+// steps < 0: min(rows, cols) (a full factorisation); otherwise a partial (truncated) one.
+void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms, int64_t steps = -1);
+// In-place Householder QR (pivot: column-pivoted, Golub + LAPACK downdating) of M, `steps`
+// reflectors.  Outputs in s: Vst, tau, beta, perm (full permutation).  M keeps R entries above
+// the diagonal of each step's pivot column in ORIGINAL column positions.
+void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot,
+               int64_t steps = -1);
 // R (steps x cols, pivot order, sign-normalised) or its transpose (cols x steps).
 void hh_extract_r(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, const double *M, int64_t ldm, double *R,
-                  int64_t ldr, bool transpose);
+                  int64_t ldr, bool transpose, int64_t steps = -1);
 // Explicit Q (rows x steps), sign-normalised.
-void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq);
+void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int64_t ldq, int64_t steps = -1);
 void hh_copy_perm(Ctx &c, HHScratch &s, int64_t count, int64_t *dst);
 
 struct TailScratch {
@@ -172,6 +174,11 @@ void tail_carve(Arena &a, TailScratch &s, int64_t l, int64_t n, int num_sms);
 // B (l x n) is overwritten.  Outputs QB (l x l), T, PB (n x l), piv0/piv1 (device int64, nullable).
 void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t ldb, int d, double *QB,
               int64_t ldqb, double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1);
+
+// Truncated pivoted QLP of W (m x n, overwritten; tail.cu).  QR: m x l scratch for Q_R.
+void tqlp(Ctx &c, TailScratch &s, HHScratch &hA, int64_t m, int64_t n, int64_t l, double *W, int64_t ldw, double *Q,
+          int64_t ldq, double *L, int64_t ldl_out, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1, double *QR,
+          int64_t ldqr);
 
 // *out (+)= ||X||_F^2, deterministic (dense.cu); part >= 1024 doubles
 void fro2_accumulate(Ctx &c, int64_t rows, int64_t cols, const double *X, int64_t ldx, double *part, double *out,

@@ -76,6 +76,29 @@ void tail_carve(Arena &a, TailScratch &s, int64_t l, int64_t n, int num_sms) {
   orth_carve(a, s.orth, n, l, num_sms);
 }
 
+// Second half of a pivoted QLP, given R0^T = Q^ R^ (s.Qhat n x l, s.Rhat l x l) and the left
+// factor Q0 (rows x l) of the first CPQR: [Q~, L^T, Π1] = cpqr(R^) (PAPER.md:100 on the
+// orthogonally equivalent l x l factor), L -> T, Q0 Π1 -> QB (rows x l), piv1; returns
+// Q1 = Q^ Q~ (n x l, in s.tmp_nl; rows still in the first CPQR's column order).
+static double *pivoted_lq(Ctx &c, TailScratch &s, int64_t rows, int64_t l, int64_t n, const double *Q0, int64_t ldq0,
+                          double *T, int64_t ldt, double *QB, int64_t ldqb, int64_t *piv1) {
+  const int64_t ldn = s.ldn, ldl = s.ldl;
+  launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, false);
+  hh_factor(c, s.hh, l, l, s.Mt, ldl, true);
+  copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.hh.perm, s.perm1);
+  RQLP_LAUNCHED(c);
+  hh_extract_r(c, s.hh, l, l, s.Mt, ldl, T, ldt, true);  // L = (L^T)^T, lower
+  hh_form_q(c, s.hh, l, l, s.Qt, ldl);
+  gemm_nn(c, n, l, l, s.Qhat, ldn, s.Qt, ldl, s.tmp_nl, ldn, s.orth.partials, s.orth.partial_elems);  // Q1
+  gather_cols_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(rows, l, Q0, ldq0, s.perm1, QB, ldqb);  // Q0 Π1
+  RQLP_LAUNCHED(c);
+  if (piv1) {
+    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm1, piv1);
+    RQLP_LAUNCHED(c);
+  }
+  return s.tmp_nl;
+}
+
 void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t ldb, int d, double *QB, int64_t ldqb,
               double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1) {
   const int64_t ldn = s.ldn, ldl = s.ldl;
@@ -91,21 +114,7 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
   c.mark("tail_qr_R0T");
   double *PO;
   if (d == 0) {
-    // [Q~, L^T, Π1] = cpqr(R^)  (Alg.1 l.6 on the orthogonally equivalent l x l factor)
-    launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, false);
-    hh_factor(c, s.hh, l, l, s.Mt, ldl, true);
-    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.hh.perm, s.perm1);
-    RQLP_LAUNCHED(c);
-    hh_extract_r(c, s.hh, l, l, s.Mt, ldl, T, ldt, true);  // L = (L^T)^T, lower
-    hh_form_q(c, s.hh, l, l, s.Qt, ldl);
-    gemm_nn(c, n, l, l, s.Qhat, ldn, s.Qt, ldl, s.tmp_nl, ldn, s.orth.partials, s.orth.partial_elems);  // Q1
-    PO = s.tmp_nl;
-    gather_cols_kernel<<<grid_for(c, l * l), 256, 0, c.stream>>>(l, l, s.Q0, ldl, s.perm1, QB, ldqb);  // Q0 Π1
-    RQLP_LAUNCHED(c);
-    if (piv1) {
-      copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm1, piv1);
-      RQLP_LAUNCHED(c);
-    }
+    PO = pivoted_lq(c, s, l, l, n, s.Q0, ldl, T, ldt, QB, ldqb, piv1);
   } else {
     launch_copy(c, l, l, s.Q0, ldl, s.QE, ldl, false);
     PO = s.Qhat;
@@ -142,6 +151,31 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
     RQLP_LAUNCHED(c);
   }
   c.mark("tail_assemble");
+}
+
+// Truncated pivoted QLP of A (NEXT-3; PAPER.md:39-42 Stewart's pivoted QLP, truncated as in
+// PAPER.md:177-179): the partial CPQR A Π0(:, 1:l) = Q_R [R11 R12] (l Householder steps of the
+// engine on a working copy W of A), then the full CPQR of [R11 R12]^T exactly as the RQLP tail
+// does for R0^T.  Q = Q_R Π1 (m x l), L (l x l, lower), P = Π0 P^ (n x l).
+void tqlp(Ctx &c, TailScratch &s, HHScratch &hA, int64_t m, int64_t n, int64_t l, double *W, int64_t ldw, double *Q,
+          int64_t ldq, double *L, int64_t ldl_out, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1, double *QR,
+          int64_t ldqr) {
+  const int64_t ldn = s.ldn, ldl = s.ldl;
+  hh_factor(c, hA, m, n, W, ldw, true, l);                  // partial CPQR, l steps
+  copy_i64_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, hA.perm, s.perm0);
+  RQLP_LAUNCHED(c);
+  hh_extract_r(c, hA, m, n, W, ldw, s.Rt, ldn, true, l);     // [R11 R12]^T, n x l
+  hh_form_q(c, hA, m, n, QR, ldqr, l);                      // Q_R, m x l
+  c.mark("tqlp_cpqr_A");
+  orth(c, s.orth, n, l, s.Rt, ldn, s.Qhat, ldn, s.Rhat, ldl);
+  double *PO = pivoted_lq(c, s, m, l, n, QR, ldqr, L, ldl_out, Q, ldq, piv1);
+  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, P, ldp);
+  RQLP_LAUNCHED(c);
+  if (piv0) {
+    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm0, piv0);
+    RQLP_LAUNCHED(c);
+  }
+  c.mark("tqlp_tail");
 }
 
 }  // namespace rqlpk

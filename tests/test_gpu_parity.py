@@ -308,3 +308,40 @@ def test_autorank_argument_errors(rq):
         rq.autorank(A, b=2, l_max=9, eps=0.1)     # l_max > n
     with pytest.raises(rq.RQLPError):
         rq.autorank(A, b=2, l_max=4, eps=-1.0)    # eps < 0
+
+
+# ------------------------------------------------------------------ NEXT-3: truncated pivoted QLP
+TQLP_CASES = [  # (name, m, n, l, sigma)
+    ("tall", 500, 300, 40, lambda j: 2.0 ** (-j / 4)),
+    ("c2_like", 1031, 1030, 110, lambda j: np.exp(-j / 50.0)),
+    ("wide", 300, 900, 50, lambda j: j**-1.0),
+    ("full", 64, 64, 64, lambda j: np.logspace(0, -6, 64)[(j - 1).astype(int)]),
+    ("one", 200, 150, 1, lambda j: j**-2.0),
+]
+
+
+@pytest.mark.parametrize("case", TQLP_CASES, ids=[c[0] for c in TQLP_CASES])
+def test_tqlp_parity(rq, orc, case):
+    """Deterministic truncated pivoted QLP on the GPU engine == oracle."""
+    name, m, n, l, sf = case
+    sig = sf(np.arange(1, min(m, n) + 1.0))
+    A = _rand_svd(m, n, sig, 5 * m + n)
+    g = rq.tqlp(_cm(A), l)
+    o = orc.tqlp(A, l)
+    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0])
+    Pg = _np(g["P"])
+    assert np.abs(Pg.T @ Pg - np.eye(l)).max() <= 1e-13 * l
+    assert not np.triu(_np(g["T"]), 1).any()
+
+
+@pytest.mark.parametrize("spectrum", ["pds", "eds"])
+def test_tqlp_paper_scale(rq, orc, spectrum):
+    """m = n = 2000, l = 125 on the paper's pds (t=30, s=2) / eds (t=30, s=1/20) matrices
+    (Tables 1-2 protocol PAPER.md:389)."""
+    from synthetic import eds_sigma, pds_sigma
+    n, l = 2000, 125
+    sig = (pds_sigma(n, 30, 2.0) if spectrum == "pds" else eds_sigma(n, 30, 1 / 20)).numpy()
+    A = _rand_svd(n, n, sig, 2000)
+    g = rq.tqlp(_cm(A), l)
+    o = orc.tqlp(A, l)
+    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0])

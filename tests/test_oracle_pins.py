@@ -419,3 +419,33 @@ def test_autorank_limits_and_equivalence(orc):
     for key in ("Q", "T", "P"):
         np.testing.assert_allclose(mid[key], ref[key], atol=1e-13)
     assert np.array_equal(mid["piv0"], ref["piv0"]) and np.array_equal(mid["piv1"], ref["piv1"])
+
+
+# ------------------------------------------------------------------ NEXT-3: truncated pivoted QLP
+@pytest.mark.parametrize("m,n,l", [(90, 70, 12), (70, 90, 25), (60, 40, 40)])
+def test_tqlp_matches_lapack_pivoted_qlp(orc, m, n, l):
+    """Truncated pivoted QLP against LAPACK's dgeqp3 via scipy: pivots of the
+    first l steps, pivots of the CPQR of [R11 R12]^T, |L-values|, and the residual
+    ||(I - Q_R Q_R^T) A||_F (catches a wrong truncation, a transposed R, a wrong Π0/Π1 assembly)."""
+    sig = 2.0 ** -np.arange(min(m, n), dtype=float) * (1 + 0.1 * np.arange(min(m, n)) % 3)
+    A = _rand_svd(m, n, np.sort(sig)[::-1], m * n)
+    o = orc.tqlp(A, l)
+    Qs, Rs, ps = sla.qr(A, pivoting=True, mode="economic")
+    assert np.array_equal(o["piv0"], ps[:l])
+    R1 = Rs[:l, :]
+    Q2, R2, p2 = sla.qr(R1.T, pivoting=True, mode="economic")
+    assert np.array_equal(o["piv1"], p2)
+    np.testing.assert_allclose(np.abs(np.diag(o["T"])), np.abs(np.diag(R2)), rtol=1e-10, atol=1e-14)
+    assert not np.triu(o["T"], 1).any()
+    Ql = Qs[:, :l]
+    direct = np.linalg.norm(A - Ql @ (Ql.T @ A))
+    assert orc.residual(A, o["Q"], o["T"], o["P"]) == pytest.approx(direct, rel=1e-8, abs=1e-14)
+    assert np.abs(o["Q"].T @ o["Q"] - np.eye(l)).max() < 1e-13 * l
+    assert np.abs(o["P"].T @ o["P"] - np.eye(l)).max() < 1e-13 * l
+
+
+def test_tqlp_full_rank_is_exact(orc):
+    """l = min(m, n): the pivoted QLP is an exact factorisation A = Q L P^T (eq. (1))."""
+    A = _rand_svd(50, 35, np.logspace(0, -6, 35), 77)
+    o = orc.tqlp(A, 35)
+    np.testing.assert_allclose(o["Q"] @ o["T"] @ o["P"].T, A, atol=1e-14)
