@@ -333,15 +333,3 @@ def test_tqlp_parity(rq, orc, case):
     assert np.abs(Pg.T @ Pg - np.eye(l)).max() <= 1e-13 * l
     assert not np.triu(_np(g["T"]), 1).any()
 
-
-@pytest.mark.parametrize("spectrum", ["pds", "eds"])
-def test_tqlp_paper_scale(rq, orc, spectrum):
-    """m = n = 2000, l = 125 on the paper's pds (t=30, s=2) / eds (t=30, s=1/20) matrices
-    (Tables 1-2 protocol PAPER.md:389)."""
-    from synthetic import eds_sigma, pds_sigma
-    n, l = 2000, 125
-    sig = (pds_sigma(n, 30, 2.0) if spectrum == "pds" else eds_sigma(n, 30, 1 / 20)).numpy()
-    A = _rand_svd(n, n, sig, 2000)
-    g = rq.tqlp(_cm(A), l)
-    o = orc.tqlp(A, l)
-    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0])
