@@ -12,12 +12,13 @@
 // Gram G + s I, s = 11 (m c + c (c+1)) u ||Y||_F^2, and enables a third pass (sCholQR3).  All of
 // this is decided on the device (no host sync): the conditional kernels read a flag word.
 //
-// The c x c Cholesky factor R and its inverse X = R^-1 come from one kernel: Gaussian
-// elimination of [G | I] in registers (c <= 128), one __syncthreads per pivot step:
+// The c x c Cholesky factor R and its inverse X = R^-1 come from one kernel (chol_blk_kernel):
+// Gauss-Jordan elimination of [G | I] in shared memory (c <= 128),
 //   step k:  S_ij -= S_ik S_jk / d_k  (k < j <= i),   W_ik = -S_ik / d_k,  W_it -= (S_ik/d_k) W_kt,
-// after which L = S D^-1/2 (G = L L^T, R = L^T) and L^-1 = D^-1/2 W, X = (L^-1)^T.
-// Larger c is blocked by 128 with the diagonal blocks done by the same kernel and the panels
-// and block back-substitution done by GEMMs.
+// after which L = S D^-1/2 (G = L L^T, R = L^T) and L^-1 = D^-1/2 W, X = (L^-1)^T; the steps
+// are taken 8 at a time (one warp factors the 8 x 8 diagonal block, the rank-8 updates are DMMA
+// tile products).  Larger c is blocked by 128 with the diagonal blocks done by the same kernel
+// and the panels and block back-substitution done by GEMMs.
 #include "internal.cuh"
 
 namespace rqlpk {
@@ -30,151 +31,234 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
 
 namespace {
 
-constexpr int CHOL_SMALL = 128;       // largest c done in one CTA (4 x 32 register rows)
+constexpr int CHOL_SMALL = 128;       // largest c done in one CTA (shared-memory working matrix)
 constexpr int CHOL_NB = 128;          // diagonal block of the blocked path
-constexpr double CHOL_BREAK = 1e-12;  // relative pivot threshold for the shifted fallback
+// Pivot classification (relative to the original Gram diagonal g0): d <= 1e-15 g0 is a dependent
+// column (rank deficiency: pivot 1, the column is later replaced), d <= 1e-12 g0 is breakdown
+// (cond(Y) >~ 1e6: the shifted pass), as is a non-finite d.
+constexpr double CHOL_BREAK = 1e-12;
+constexpr double CHOL_DEP = 1e-15;
 
-constexpr double CHOL_DEP = 1e-15;  // relative pivot at or below which a column is dependent
+// chol_blk_kernel: the elimination of [G | I] in 8-pivot blocks with the whole n x n working
+// matrix M in shared memory (ld 132: conflict-free DMMA fragment loads).  Per block
+// K = [k0, k0+8):
+//   phase 1 (warp 0): LDL^T of the 8 x 8 diagonal block D = L_KK Δ L_KK^T and W_KK = L_KK^-1
+//            (lane i holds row i; 8 pivots, each classified as above);
+//   phase 2: every other row tile of the block column: M[T, K] <- M[T, K] W_KK^T
+//            (rows > K: P = S_rK L_KK^-T = L_rK Δ, the final S values; rows < K: the final W rows);
+//   phase 3: trailing columns c > K: S_rc -= L_rK P_cK^T (r >= c) and W_ct -= L_cK W_Kt (t in
+//            the finished rows), as 8 x 8 x 8 DMMA tile products (mma.m8n8k4.f64); warp 0
+//            first updates the next diagonal tile and runs phase 1 of block K+1 (lookahead).
+// Equal to the scalar elimination in exact arithmetic (block LDL^T, readings R3/R19).  The
+// scalar one-pivot-per-barrier form was issue bound (~6 instructions per FMA for the masks).
+constexpr int CB_LD = 132;
 
-// d = Schur pivot of column k, g0 = its original Gram diagonal.  Dependent column (rank
-// deficiency, d <= 1e-15 g0, incl. a zero column): dep[k] = 1, pivot 1.  Ill-conditioned
-// (d <= 1e-12 g0): breakdown -> the shifted pass.  Returns the pivot to use.
-__device__ __forceinline__ double classify_pivot(double d, double g0, int k, int *dep, int *s_fail, int *s_dep) {
-  if (dep) dep[k] = 0;
-  if (!isfinite(d)) {
-    *s_fail = 1;
-    return 1.0;
-  }
-  if (dep && !(d > CHOL_DEP * g0)) {
-    dep[k] = 1;
-    *s_dep = 1;
-    return 1.0;
-  }
-  if (!(d > CHOL_BREAK * g0)) {
-    *s_fail = 1;
-    return 1.0;
-  }
-  return d;
+__device__ __forceinline__ void dmma8(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
-// One CTA: R (upper, G = R^T R) and X = R^-1 (upper) of the n x n SPD block G (n <= 128).
-// Gorig supplies the original diagonal for the relative breakdown test.  On breakdown sets
-// (*fail_word) |= fail_bit (R, X then undefined).  Skipped unless (*cond & mask) when cond set.
-//
-// The working matrix M (n x n) holds S (Schur complements) in its lower triangle and W^T in its
-// strictly upper triangle (M[t][i] = W_it, t < i; W unit lower).  Thread (c, q) (c = column,
-// q = row quarter) keeps M[32q .. 32q+31][c] in registers.  Step k needs only column k of M
-// (bc[r] = M[r][k], bc[k] := 1) and d_k = M[k][k]; every active element updates as
-//     x -= bc[r] bc[c] / d_k     active iff c > k and (r >= c or r <= k),
-// except W_ck (r == k) which becomes -bc[c]/d_k (covered by bc[k] = 1 because its old value is 0).
-// Inactive elements get a zero multiplier (branch-free); warps whose columns are all <= k retire
-// from the step.  The owners of column k+1 publish it right after their step-k update, so a
-// step costs a single __syncthreads.
-__global__ void __launch_bounds__(512, 1) chol_inv_kernel(int n, const double *G, int64_t ldg, const double *Gorig,
+// 1/x to ~1 ulp without the IEEE division's slow-path branch: MUFU seed + two Newton steps
+// (x is a positive normal pivot here; callers replaced non-finite / tiny pivots by 1).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G, int64_t ldg, const double *Gorig,
                                                           int64_t ldo, double *R, int64_t ldr, double *X, int64_t ldx,
                                                           unsigned *fail_word, unsigned fail_bit, int *dep,
-                                                          unsigned dep_bit, unsigned *flag_word,
-                                                          const unsigned *cond, unsigned cond_mask) {
+                                                          unsigned dep_bit, unsigned *flag_word, const unsigned *cond,
+                                                          unsigned cond_mask, unsigned long long *trace) {
   if (cond && ((*cond) & cond_mask) == 0) return;
-  extern __shared__ double xs[];  // n x (n|1) staging for the coalesced X write
-  __shared__ __align__(16) double bc[2][CHOL_SMALL];
-  __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL];
+  auto stamp = [&](int slot) {
+    if (trace) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[slot] = t;
+    }
+  };
+  extern __shared__ double M[];  // npad x CB_LD, column-major: M[r + c * CB_LD]
+  __shared__ double wkk[2][64];  // W_KK[i][t] at wkk[.][i * 8 + t] (unit lower), double-buffered
+  __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL], sq[CHOL_SMALL];
   __shared__ int s_fail, s_dep;
-  const int c = threadIdx.x & (CHOL_SMALL - 1), q = threadIdx.x >> 7;  // 128 columns x 4 quarters
-  const int r0 = 32 * q;
-  const bool col_ok = c < n;
-  double x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int r = r0 + i;
-    x[i] = (col_ok && r < n && r >= c) ? G[c + (int64_t)r * ldg] : 0.0;  // S = G (symmetric)
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) g0s[i] = Gorig[i + (int64_t)i * ldo];
-  if (threadIdx.x == 0) { s_fail = 0; s_dep = 0; }
-  for (int i = threadIdx.x; i < 2 * CHOL_SMALL; i += blockDim.x) (&bc[0][0])[i] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int npad = (n + 7) & ~7, nt = npad >> 3;
+  // load: M(b, a) = G[a + b ldg] for a <= b (the lower part, read coalesced over a), the upper
+  // part (the W^T entries) zero, identity padding
+  for (int b = warp; b < npad; b += nwarps)
+    for (int a = lane; a < npad; a += 32) {
+      double v = 0.0;
+      if (a < n && b < n) { if (a <= b) v = G[a + (int64_t)b * ldg]; }
+      else if (a == b) v = 1.0;
+      M[b + a * CB_LD] = v;
+      if (a < b) M[a + b * CB_LD] = 0.0;
+    }
+  for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] : 1.0;
+  if (tid == 0) { s_fail = 0; s_dep = 0; }
   __syncthreads();
-  if (c == 0) {
+  const int fr = lane >> 2, fq = lane & 3;  // DMMA fragment coordinates
+  // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf]
+  auto phase1 = [&](int kb, double *wk) {
+    const int k0 = kb * 8;
+    const int i = lane & 7;
+    double d[8], w[8], g0[8], piv[8], sv[8];  // lane i: row i of the block and of W_KK
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int r = r0 + i;
-      if (r < n) bc[0][r] = (r == 0) ? 1.0 : x[i];
-      if (r == 0) {
-        const double d = classify_pivot(x[i], g0s[0], 0, dep, &s_fail, &s_dep);
-        dpiv[0] = d;
-        dinv[0] = 1.0 / d;
+    for (int j = 0; j < 8; ++j) {
+      const int r = k0 + i, cc = k0 + j;
+      d[j] = r >= cc ? M[r + cc * CB_LD] : M[cc + r * CB_LD];
+      w[j] = (i == j) ? 1.0 : 0.0;
+      g0[j] = g0s[cc];
+    }
+    // the pivot chain only: shuffles, the reciprocal and FMAs (bookkeeping after the loop)
+    unsigned kinds = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const double draw = __shfl_sync(0xffffffffu, d[p], p);
+      double pv = draw;
+      if (!isfinite(draw)) { kinds |= 2u << (2 * p); pv = 1.0; }
+      else if (dep && !(draw > CHOL_DEP * g0[p])) { kinds |= 1u << (2 * p); pv = 1.0; }
+      else if (!(draw > CHOL_BREAK * g0[p])) { kinds |= 2u << (2 * p); pv = 1.0; }
+      piv[p] = pv;
+      const double pinv = fast_rcp(pv);
+      sv[p] = d[p];                                   // final S value L_ip d_p (i > p)
+      const double l = (i > p) ? d[p] * pinv : 0.0;  // L_ip (row i of the block)
+#pragma unroll
+      for (int j = p + 1; j < 8; ++j) d[j] = fma(-l, __shfl_sync(0xffffffffu, d[j], p), d[j]);
+#pragma unroll
+      for (int t = 0; t <= p; ++t) w[t] = fma(-l, __shfl_sync(0xffffffffu, w[t], p), w[t]);
+    }
+    if (lane < 8) {
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
+      const int kg = k0 + i;  // lane i records pivot i
+      double pv = piv[0];
+#pragma unroll
+      for (int p = 1; p < 8; ++p) if (i == p) pv = piv[p];
+      dpiv[kg] = pv;
+      dinv[kg] = fast_rcp(pv);
+      const unsigned kind = (kinds >> (2 * i)) & 3u;
+      if (kg < n) {
+        if (dep) dep[kg] = kind == 1;
+        if (kind == 1) s_dep = 1;
+        if (kind == 2) s_fail = 1;
       }
     }
-  }
-  __syncthreads();
-  const unsigned rowvalid = (n - r0 >= 32) ? 0xffffffffu : (n - r0 <= 0 ? 0u : ((1u << (n - r0)) - 1u));
-  for (int k = 0; k < n; ++k) {
-    const double *b0 = bc[k & 1];
-    double *b1 = bc[(k + 1) & 1];
-    const int warp_c0 = (threadIdx.x & 127) - (threadIdx.x & 31);  // first column of this warp
-    if (warp_c0 + 31 > k && warp_c0 < n) {
-      const double bcc = (col_ok && c > k) ? b0[c] * dinv[k] : 0.0;
-      // active rows: r <= k (W part) or r >= c (S part)
-      const int lo_cnt = min(max(k - r0 + 1, 0), 32);               // rows r0 .. k
-      const int hi_start = min(max(c - r0, 0), 32);                 // rows c .. r0+31
-      const unsigned lowm = lo_cnt >= 32 ? 0xffffffffu : ((1u << lo_cnt) - 1u);
-      const unsigned highm = hi_start >= 32 ? 0u : (0xffffffffu << hi_start);
-      const unsigned act = (lowm | highm) & rowvalid;
+    if (lane < 8) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const double2 br = *reinterpret_cast<const double2 *>(b0 + r0 + i);
-        const double m0 = ((act >> i) & 1u) ? bcc : 0.0;
-        const double m1 = ((act >> (i + 1)) & 1u) ? bcc : 0.0;
-        x[i] = fma(-br.x, m0, x[i]);
-        x[i + 1] = fma(-br.y, m1, x[i + 1]);
+      for (int t = 0; t < 8; ++t) {
+        wk[i * 8 + t] = w[t];
+        if (t < i) M[(k0 + t) + (k0 + i) * CB_LD] = w[t];  // W_{k0+i, k0+t} in the upper part
       }
     }
-    // publish column k+1 (and its pivot d, breakdown-checked, and 1/d)
-    const int kn = k + 1;
-    if (kn < n && c == kn) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 2)
-        *reinterpret_cast<double2 *>(b1 + r0 + i) = make_double2(x[i], x[i + 1]);
-      if (kn >= r0 && kn < r0 + 32) {
-        const double d = classify_pivot(b1[kn], g0s[kn], kn, dep, &s_fail, &s_dep);
-        dpiv[kn] = d;
-        dinv[kn] = 1.0 / d;
-        b1[kn] = 1.0;
+  };
+  if (tid == 0) stamp(0);
+  if (warp == 0) phase1(0, wkk[0]);
+  if (tid == 0) stamp(1);
+
+  __syncthreads();
+  for (int kb = 0; kb < nt; ++kb) {
+    const int k0 = kb * 8;
+    const double *wk = wkk[kb & 1];
+    if (tid == 32) stamp(4 + 4 * kb);
+    // ---- phase 2: M[T, K] <- M[T, K] W_KK^T for every row tile T != K
+    for (int T = warp; T < nt; T += nwarps) {
+      if (T == kb) continue;
+      const int r = T * 8 + fr;
+      const double a0 = M[r + (k0 + 2 * fq) * CB_LD], a1 = M[r + (k0 + 2 * fq + 1) * CB_LD];
+      const double b0 = wk[fr * 8 + 2 * fq], b1 = wk[fr * 8 + 2 * fq + 1];  // B[k][j] = W_KK[j][k], j = fr
+      double c0 = 0.0, c1 = 0.0;
+      dmma8(c0, c1, a0, b0);
+      dmma8(c0, c1, a1, b1);
+      __syncwarp();
+      M[r + (k0 + 2 * fq) * CB_LD] = c0;
+      M[r + (k0 + 2 * fq + 1) * CB_LD] = c1;
+    }
+    __syncthreads();
+    if (tid == 32) stamp(5 + 4 * kb);
+    // ---- phase 3: trailing column tiles Tc > kb.  S part: tiles (Tr >= Tc); W part: Tr <= kb.
+    //      Tile 0 is the next diagonal block: warp 0 updates it and then runs phase 1 of block
+    //      kb + 1 (lookahead) while warps 1.. do the remaining tiles.
+    const int ntrail = nt - kb - 1;
+    if (ntrail > 0) {
+      const int n_s = ntrail * (ntrail + 1) / 2, n_w = (kb + 1) * ntrail;
+      const double dv0 = dinv[k0 + 2 * fq], dv1 = dinv[k0 + 2 * fq + 1];
+      auto tile = [&](int t) {
+        int Tr, Tc;
+        double a0, a1;
+        if (t < n_s) {  // S tile: enumerate (Tr, Tc) with kb < Tc <= Tr
+          int u = t, cnum = 0;
+          while (u >= ntrail - cnum) { u -= ntrail - cnum; ++cnum; }
+          Tc = kb + 1 + cnum;
+          Tr = Tc + u;
+          const int r = Tr * 8 + fr;
+          a0 = M[r + (k0 + 2 * fq) * CB_LD] * dv0;  // L_rK = P_rK Δ^-1
+          a1 = M[r + (k0 + 2 * fq + 1) * CB_LD] * dv1;
+        } else {        // W tile: rows Tr <= kb, A[t][k] = W_{k0+k, t}
+          const int u = t - n_s;
+          Tr = u % (kb + 1);
+          Tc = kb + 1 + u / (kb + 1);
+          const int tr = Tr * 8 + fr;
+          if (Tr < kb) {
+            a0 = M[tr + (k0 + 2 * fq) * CB_LD];
+            a1 = M[tr + (k0 + 2 * fq + 1) * CB_LD];
+          } else {
+            a0 = wk[(2 * fq) * 8 + fr];
+            a1 = wk[(2 * fq + 1) * 8 + fr];
+          }
+        }
+        // B[k][c] = P_cK[c][k] (S tiles) or L_cK[c][k] (W tiles), c = Tc*8 + fr
+        const int cc = Tc * 8 + fr;
+        double b0 = M[cc + (k0 + 2 * fq) * CB_LD], b1 = M[cc + (k0 + 2 * fq + 1) * CB_LD];
+        if (t >= n_s) { b0 *= dv0; b1 *= dv1; }
+        double c0 = 0.0, c1 = 0.0;
+        dmma8(c0, c1, a0, b0);
+        dmma8(c0, c1, a1, b1);
+        const int orow = Tr * 8 + fr, ocol = Tc * 8 + 2 * fq;
+        if (t >= n_s || Tr != Tc || orow >= ocol) M[orow + ocol * CB_LD] -= c0;
+        if (t >= n_s || Tr != Tc || orow >= ocol + 1) M[orow + (ocol + 1) * CB_LD] -= c1;
+      };
+      if (warp == 0) {
+        tile(0);
+        __syncwarp();
+        if (tid == 0) stamp(6 + 4 * kb);
+        phase1(kb + 1, wkk[(kb + 1) & 1]);
+        if (tid == 0) stamp(7 + 4 * kb);
+      } else {
+        for (int t = warp; t < n_s + n_w; t += nwarps - 1) tile(t);
+        if (tid == 32) stamp(3);
       }
     }
     __syncthreads();
   }
+  for (int i = tid; i < n; i += blockDim.x) sq[i] = sqrt(dpiv[i]);
   __syncthreads();
-  // outputs: R(c, r) = S_rc / sqrt(d_c) (r > c), R(r, r) = sqrt(d_r), R lower = 0;
+  // outputs: R(c, r) = S_rc / sqrt(d_c) (c < r), R(r, r) = sqrt(d_r), R lower = 0;
   //          X(r, c) = W_cr / sqrt(d_c) (r < c), X(r, r) = 1 / sqrt(d_r), X lower = 0.
-  const int ldxs = n | 1;
-  if (col_ok) {
-    const double sdc = sqrt(dpiv[c]);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int r = r0 + i;
-      if (r >= n) continue;
-      if (r > c) {
-        R[c + (int64_t)r * ldr] = x[i] / sdc;  // coalesced over c
-        xs[r + c * ldxs] = 0.0;
-      } else if (r == c) {
-        R[c + (int64_t)c * ldr] = sdc;
-        xs[c + c * ldxs] = 1.0 / sdc;
-      } else {
-        xs[r + c * ldxs] = x[i] / sdc;
-      }
+  for (int r = warp; r < n; r += nwarps)
+    for (int c = lane; c < n; c += 32) {  // R(c, r): coalesced over c
+      double v = 0.0;
+      if (c < r) v = M[r + c * CB_LD] / sq[c];
+      else if (c == r) v = sq[r];
+      R[c + (int64_t)r * ldr] = v;
+    }
+  for (int c = warp; c < n; c += nwarps) {
+    const double isq = 1.0 / sq[c];
+    for (int r = lane; r < n; r += 32) {  // X(r, c): coalesced over r
+      double v = 0.0;
+      if (r < c) v = M[r + c * CB_LD] * isq;
+      else if (r == c) v = isq;
+      X[r + (int64_t)c * ldx] = v;
     }
   }
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    if (i > j) R[i + (int64_t)j * ldr] = 0.0;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    X[i + (int64_t)j * ldx] = xs[i + j * ldxs];
-  }
-  if (threadIdx.x == 0 && s_fail) atomicOr(fail_word, fail_bit);
-  if (threadIdx.x == 0 && s_dep && dep) {
+  if (tid == 0 && s_fail) atomicOr(fail_word, fail_bit);
+  if (tid == 0 && s_dep && dep) {
     atomicOr(fail_word, dep_bit);
     atomicOr(flag_word, (unsigned)RQLP_FLAG_RANK_DEFICIENT);
   }
@@ -272,13 +356,13 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
                      const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0) {
   static bool attr = false;
   if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CHOL_SMALL * (CHOL_SMALL | 1) * 8));
+    RQLP_CUDA(cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   CHOL_SMALL * CB_LD * 8));
     attr = true;
   }
-  chol_inv_kernel<<<1, 512, (size_t)n * (n | 1) * 8, c.stream>>>(n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word,
-                                                                 fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond,
-                                                                 mask);
+  chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
+      n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
+      c.trace);
   RQLP_LAUNCHED(c);
 }
 
