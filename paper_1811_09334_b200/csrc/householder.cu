@@ -102,7 +102,7 @@ __device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
   return ((unsigned long long)hi << 32) | tag;
 }
 
-// Shared-memory layout: vraw[rows] | vn1[owned] | vn2[owned] | colbuf[owned*rows] (SMEMC) | done_l[owned]
+// Shared-memory layout: vraw[rows] | vn1[owned] | rvn2[owned] | colbuf[owned*rows] (SMEMC) | done_l[owned]
 //
 // Per step: (GRID only) warp 0 polls the tagged records (the exchange is the grid barrier), all
 // threads fetch the winner's rows j.. into vraw, one __syncthreads; then EVERY warp recomputes
@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   extern __shared__ double smem[];
   double *vraw = smem;
   double *vn1 = vraw + a.rows;
-  double *vn2 = vn1 + a.owned_max;
-  double *colbuf = vn2 + a.owned_max;
+  double *rvn2 = vn1 + a.owned_max;  // 1 / (squared norm at the last recompute)
+  double *colbuf = rvn2 + a.owned_max;
   int *done_l = reinterpret_cast<int *>(colbuf + (SMEMC ? (int64_t)a.owned_max * a.rows : 0));
   __shared__ double s_bv[2][32];
   __shared__ int s_bi[2][32];
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   if (a.pivot)
     for (int li = warp; li < nown; li += wpb) {
       double nrm = warp_sumsq(colptr(li), rows);  // squared norms (monotone: same argmax)
-      if (lane == 0) { vn1[li] = nrm; vn2[li] = nrm; }
+      if (lane == 0) { vn1[li] = nrm; rvn2[li] = nrm != 0.0 ? 1.0 / nrm : 0.0; }
       if (better(nrm, b + li * G, best.v, best.i)) { best.v = nrm; best.i = b + li * G; }
     }
   {
@@ -259,9 +259,9 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
     if (xn2 == 0.0) {
       tau = 0.0; beta = alpha; scal = 0.0;
     } else {
-      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+      beta = -copysign(fast_sqrt(fma(alpha, alpha, xn2)), alpha);
       const double amb = alpha - beta;              // tau = (beta - alpha)/beta, scal = 1/(alpha - beta)
-      const double rinv = 1.0 / (beta * amb);       // one division for both
+      const double rinv = fast_rcp(beta * amb);     // one reciprocal for both
       tau = -amb * amb * rinv;
       scal = beta * rinv;
     }
@@ -286,35 +286,50 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
       for (int li = warp * 4 + g8; li < nown; li += wpb * 4) {
         const int gi = b + li * G;
         if (gi == p || done_l[li]) continue;
+        // downdating operands first (off the dependency chain): 1/vn1 and vn1/vn2 (rvn2 = 1/vn2)
+        double n1 = 0.0, rn1 = 0.0, q12 = 0.0;
+        if (a.pivot) {
+          n1 = vn1[li];
+          if (n1 != 0.0) {
+            rn1 = fast_rcp(n1);
+            q12 = n1 * rvn2[li];
+          }
+        }
         double *col = colptr(li) + j;
+        double x = col[0];
         if (tau != 0.0) {
-          double w = l8 == 0 ? col[0] : 0.0;
-          for (int r = 1 + l8; r < len; r += 8) w = fma(cp[r] * scal, col[r], w);
+          double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;  // two chains of the dot product
+          int r = 1 + l8;
+          for (; r + 8 < len; r += 16) {
+            w0 = fma(cp[r] * scal, col[r], w0);
+            w1 = fma(cp[r + 8] * scal, col[r + 8], w1);
+          }
+          if (r < len) w0 = fma(cp[r] * scal, col[r], w0);
+          double w = w0 + w1;
           w += __shfl_xor_sync(gmask, w, 4);
           w += __shfl_xor_sync(gmask, w, 2);
           w += __shfl_xor_sync(gmask, w, 1);
           w *= tau;
-          if (l8 == 0) col[0] -= w;
-          for (int r = 1 + l8; r < len; r += 8) col[r] = fma(-w, cp[r] * scal, col[r]);
+          x -= w;  // the updated row-j entry (identical in the 8 lanes)
+          if (l8 == 0) col[0] = x;
+          for (int rr = 1 + l8; rr < len; rr += 8) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
           __syncwarp(gmask);
         }
         if (a.pivot) {
           // xLAQP2 downdating on squared norms (vn1 = ||.||^2, vn2 = ||.||^2 at the last
           // recompute): t = 1 - x^2/vn1, recompute when t vn1/vn2 <= tol3z.
-          double n1 = vn1[li];
           if (n1 != 0.0) {
-            const double x = col[0];
-            double t = 1.0 - (x * x) / n1;
+            double t = fma(-x * x, rn1, 1.0);
             t = t < 0.0 ? 0.0 : t;
-            const double t2 = t * n1 / vn2[li];
+            const double t2 = t * q12;
             if (t2 <= TOL3Z) {
               double ss = 0.0;
-              for (int r = 1 + l8; r < len; r += 8) ss = fma(col[r], col[r], ss);
+              for (int rr = 1 + l8; rr < len; rr += 8) ss = fma(col[rr], col[rr], ss);
               ss += __shfl_xor_sync(gmask, ss, 4);
               ss += __shfl_xor_sync(gmask, ss, 2);
               ss += __shfl_xor_sync(gmask, ss, 1);
               n1 = (j + 1 < rows) ? ss : 0.0;
-              if (l8 == 0) vn2[li] = n1;
+              if (l8 == 0) rvn2[li] = n1 != 0.0 ? 1.0 / n1 : 0.0;
             } else {
               n1 = n1 * t;
             }
@@ -478,7 +493,12 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     RQLP_LAUNCHED(c);
   } else {
     // enough CTAs that each owns >= 8 columns (fewer records to exchange), at most one per SM
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(c.num_sms, s.max_slots), ceil_div(cols, 8)));
+    static int per_cta = -1;
+    if (per_cta < 0) {
+      const char *e = getenv("RQLP_ENGINE_COLS");
+      per_cta = e ? std::max(1, atoi(e)) : 8;
+    }
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(c.num_sms, s.max_slots), ceil_div(cols, per_cta)));
     const int64_t owned = ceil_div(cols, G);
     const bool cached = smem_for(owned, true) <= SMEM_MAX;
     if (!cached && smem_for(owned, false) > SMEM_MAX) throw std::runtime_error("hh_factor: too many rows");

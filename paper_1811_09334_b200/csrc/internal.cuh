@@ -46,6 +46,31 @@ static inline bool sync_debug() {
   } while (0)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+#ifdef __CUDACC__
+// 1/x and sqrt(x) to ~1 ulp without the IEEE routines' slow-path branches: MUFU seed + Newton
+// steps (x positive and normal; callers handle zero / non-finite values before).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  // y ~ x^-1/2: two Newton steps on y, then s = x y with one correction (Markstein)
+  double h = 0.5 * y;
+  double g = x * y;
+  double e = fma(-g, h, 0.5);
+  g = fma(g, e, g);
+  h = fma(h, e, h);
+  e = fma(-g, g, x);
+  return fma(e, h, g);
+}
+#endif
 static inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // Device-side flag words (one per handle, in the workspace).

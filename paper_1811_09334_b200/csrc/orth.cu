@@ -59,182 +59,208 @@ __device__ __forceinline__ void dmma8(double &d0, double &d1, double a, double b
       : "d"(a), "d"(b));
 }
 
-// 1/x to ~1 ulp without the IEEE division's slow-path branch: MUFU seed + two Newton steps
-// (x is a positive normal pivot here; callers replaced non-finite / tiny pivots by 1).
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G, int64_t ldg, const double *Gorig,
                                                           int64_t ldo, double *R, int64_t ldr, double *X, int64_t ldx,
                                                           unsigned *fail_word, unsigned fail_bit, int *dep,
                                                           unsigned dep_bit, unsigned *flag_word, const unsigned *cond,
-                                                          unsigned cond_mask, unsigned long long *trace) {
+                                                          unsigned cond_mask, int near_id, double shift_m,
+                                                          unsigned *shift_word, unsigned shift_bit) {
   if (cond && ((*cond) & cond_mask) == 0) return;
-  auto stamp = [&](int slot) {
-    if (trace) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[slot] = t;
-    }
-  };
   extern __shared__ double M[];  // npad x CB_LD, column-major: M[r + c * CB_LD]
   __shared__ double wkk[2][64];  // W_KK[i][t] at wkk[.][i * 8 + t] (unit lower), double-buffered
   __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL], sq[CHOL_SMALL];
+  __shared__ double red[16];
   __shared__ int s_fail, s_dep;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int npad = (n + 7) & ~7, nt = npad >> 3;
-  // load: M(b, a) = G[a + b ldg] for a <= b (the lower part, read coalesced over a), the upper
-  // part (the W^T entries) zero, identity padding
-  for (int b = warp; b < npad; b += nwarps)
-    for (int a = lane; a < npad; a += 32) {
-      double v = 0.0;
-      if (a < n && b < n) { if (a <= b) v = G[a + (int64_t)b * ldg]; }
-      else if (a == b) v = 1.0;
-      M[b + a * CB_LD] = v;
-      if (a < b) M[a + b * CB_LD] = 0.0;
+  if (near_id) {
+    // CholeskyQR2's second pass: if max |G - I| <= 2^-27, R = I + triu(E,1) + diag(E)/2 and
+    // X = I - (same) are exact to below u (the neglected terms are O(|E|^2))
+    double emax = 0.0;
+    for (int b = warp; b < n; b += nwarps)
+      for (int a = lane; a < n; a += 32) emax = fmax(emax, fabs(G[a + (int64_t)b * ldg] - (a == b ? 1.0 : 0.0)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    if (lane == 0) red[warp] = emax;
+    __syncthreads();
+    double mx = 0.0;
+    for (int w = 0; w < nwarps; ++w) mx = fmax(mx, red[w]);
+    if (mx <= 0x1p-27) {
+      for (int b = warp; b < n; b += nwarps)
+        for (int a = lane; a < n; a += 32) {
+          const double g = G[a + (int64_t)b * ldg];
+          double u = 0.0;
+          if (a < b) u = g;
+          else if (a == b) u = 0.5 * (g - 1.0);
+          R[a + (int64_t)b * ldr] = (a == b ? 1.0 : 0.0) + u;
+          X[a + (int64_t)b * ldx] = (a == b ? 1.0 : 0.0) - u;
+        }
+      return;
     }
-  for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] : 1.0;
+  }
+  // shift > 0: the retry after a breakdown (shifted CholeskyQR, G + shift I); dep detection off
+  auto load = [&](double shift) {
+    // M(b, a) = G[a + b ldg] for a <= b (the lower part, read coalesced over a), the upper part
+    // (the W^T entries) zero, identity padding
+    for (int b = warp; b < npad; b += nwarps)
+      for (int a = lane; a < npad; a += 32) {
+        double v = 0.0;
+        if (a < n && b < n) { if (a <= b) v = G[a + (int64_t)b * ldg] + (a == b ? shift : 0.0); }
+        else if (a == b) v = 1.0;
+        M[b + a * CB_LD] = v;
+        if (a < b) M[a + b * CB_LD] = 0.0;
+      }
+    for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
+  };
+  load(0.0);
   if (tid == 0) { s_fail = 0; s_dep = 0; }
   __syncthreads();
-  const int fr = lane >> 2, fq = lane & 3;  // DMMA fragment coordinates
-  // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf]
-  auto phase1 = [&](int kb, double *wk) {
-    const int k0 = kb * 8;
-    const int i = lane & 7;
-    double d[8], w[8], g0[8], piv[8], sv[8];  // lane i: row i of the block and of W_KK
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int r = k0 + i, cc = k0 + j;
-      d[j] = r >= cc ? M[r + cc * CB_LD] : M[cc + r * CB_LD];
-      w[j] = (i == j) ? 1.0 : 0.0;
-      g0[j] = g0s[cc];
-    }
-    // the pivot chain only: shuffles, the reciprocal and FMAs (bookkeeping after the loop)
-    unsigned kinds = 0;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const double draw = __shfl_sync(0xffffffffu, d[p], p);
-      double pv = draw;
-      if (!isfinite(draw)) { kinds |= 2u << (2 * p); pv = 1.0; }
-      else if (dep && !(draw > CHOL_DEP * g0[p])) { kinds |= 1u << (2 * p); pv = 1.0; }
-      else if (!(draw > CHOL_BREAK * g0[p])) { kinds |= 2u << (2 * p); pv = 1.0; }
-      piv[p] = pv;
-      const double pinv = fast_rcp(pv);
-      sv[p] = d[p];                                   // final S value L_ip d_p (i > p)
-      const double l = (i > p) ? d[p] * pinv : 0.0;  // L_ip (row i of the block)
-#pragma unroll
-      for (int j = p + 1; j < 8; ++j) d[j] = fma(-l, __shfl_sync(0xffffffffu, d[j], p), d[j]);
-#pragma unroll
-      for (int t = 0; t <= p; ++t) w[t] = fma(-l, __shfl_sync(0xffffffffu, w[t], p), w[t]);
-    }
-    if (lane < 8) {
-#pragma unroll
-      for (int p = 0; p < 8; ++p)
-        if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
-      const int kg = k0 + i;  // lane i records pivot i
-      double pv = piv[0];
-#pragma unroll
-      for (int p = 1; p < 8; ++p) if (i == p) pv = piv[p];
-      dpiv[kg] = pv;
-      dinv[kg] = fast_rcp(pv);
-      const unsigned kind = (kinds >> (2 * i)) & 3u;
-      if (kg < n) {
-        if (dep) dep[kg] = kind == 1;
-        if (kind == 1) s_dep = 1;
-        if (kind == 2) s_fail = 1;
+  int *dep_att = dep;
+  for (int attempt = 0;; ++attempt) {
+    const int fr = lane >> 2, fq = lane & 3;  // DMMA fragment coordinates
+    // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf]
+    auto phase1 = [&](int kb, double *wk) {
+      const int k0 = kb * 8;
+      const int i = lane & 7;
+      double d[8], w[8], g0[8], piv[8], sv[8];  // lane i: row i of the block and of W_KK
+  #pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = k0 + i, cc = k0 + j;
+        d[j] = r >= cc ? M[r + cc * CB_LD] : M[cc + r * CB_LD];
+        w[j] = (i == j) ? 1.0 : 0.0;
+        g0[j] = g0s[cc];
       }
-    }
-    if (lane < 8) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        wk[i * 8 + t] = w[t];
-        if (t < i) M[(k0 + t) + (k0 + i) * CB_LD] = w[t];  // W_{k0+i, k0+t} in the upper part
+      // the pivot chain only: shuffles, the reciprocal and FMAs (bookkeeping after the loop)
+      unsigned kinds = 0;
+  #pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const double draw = __shfl_sync(0xffffffffu, d[p], p);
+        double pv = draw;
+        if (!isfinite(draw)) { kinds |= 2u << (2 * p); pv = 1.0; }
+        else if (dep_att && !(draw > CHOL_DEP * g0[p])) { kinds |= 1u << (2 * p); pv = 1.0; }
+        else if (!(draw > CHOL_BREAK * g0[p])) { kinds |= 2u << (2 * p); pv = 1.0; }
+        piv[p] = pv;
+        const double pinv = fast_rcp(pv);
+        sv[p] = d[p];                                   // final S value L_ip d_p (i > p)
+        const double l = (i > p) ? d[p] * pinv : 0.0;  // L_ip (row i of the block)
+  #pragma unroll
+        for (int j = p + 1; j < 8; ++j) d[j] = fma(-l, __shfl_sync(0xffffffffu, d[j], p), d[j]);
+  #pragma unroll
+        for (int t = 0; t <= p; ++t) w[t] = fma(-l, __shfl_sync(0xffffffffu, w[t], p), w[t]);
       }
-    }
-  };
-  if (tid == 0) stamp(0);
-  if (warp == 0) phase1(0, wkk[0]);
-  if (tid == 0) stamp(1);
-
-  __syncthreads();
-  for (int kb = 0; kb < nt; ++kb) {
-    const int k0 = kb * 8;
-    const double *wk = wkk[kb & 1];
-    if (tid == 32) stamp(4 + 4 * kb);
-    // ---- phase 2: M[T, K] <- M[T, K] W_KK^T for every row tile T != K
-    for (int T = warp; T < nt; T += nwarps) {
-      if (T == kb) continue;
-      const int r = T * 8 + fr;
-      const double a0 = M[r + (k0 + 2 * fq) * CB_LD], a1 = M[r + (k0 + 2 * fq + 1) * CB_LD];
-      const double b0 = wk[fr * 8 + 2 * fq], b1 = wk[fr * 8 + 2 * fq + 1];  // B[k][j] = W_KK[j][k], j = fr
-      double c0 = 0.0, c1 = 0.0;
-      dmma8(c0, c1, a0, b0);
-      dmma8(c0, c1, a1, b1);
-      __syncwarp();
-      M[r + (k0 + 2 * fq) * CB_LD] = c0;
-      M[r + (k0 + 2 * fq + 1) * CB_LD] = c1;
-    }
-    __syncthreads();
-    if (tid == 32) stamp(5 + 4 * kb);
-    // ---- phase 3: trailing column tiles Tc > kb.  S part: tiles (Tr >= Tc); W part: Tr <= kb.
-    //      Tile 0 is the next diagonal block: warp 0 updates it and then runs phase 1 of block
-    //      kb + 1 (lookahead) while warps 1.. do the remaining tiles.
-    const int ntrail = nt - kb - 1;
-    if (ntrail > 0) {
-      const int n_s = ntrail * (ntrail + 1) / 2, n_w = (kb + 1) * ntrail;
-      const double dv0 = dinv[k0 + 2 * fq], dv1 = dinv[k0 + 2 * fq + 1];
-      auto tile = [&](int t) {
-        int Tr, Tc;
-        double a0, a1;
-        if (t < n_s) {  // S tile: enumerate (Tr, Tc) with kb < Tc <= Tr
-          int u = t, cnum = 0;
-          while (u >= ntrail - cnum) { u -= ntrail - cnum; ++cnum; }
-          Tc = kb + 1 + cnum;
-          Tr = Tc + u;
-          const int r = Tr * 8 + fr;
-          a0 = M[r + (k0 + 2 * fq) * CB_LD] * dv0;  // L_rK = P_rK Δ^-1
-          a1 = M[r + (k0 + 2 * fq + 1) * CB_LD] * dv1;
-        } else {        // W tile: rows Tr <= kb, A[t][k] = W_{k0+k, t}
-          const int u = t - n_s;
-          Tr = u % (kb + 1);
-          Tc = kb + 1 + u / (kb + 1);
-          const int tr = Tr * 8 + fr;
-          if (Tr < kb) {
-            a0 = M[tr + (k0 + 2 * fq) * CB_LD];
-            a1 = M[tr + (k0 + 2 * fq + 1) * CB_LD];
-          } else {
-            a0 = wk[(2 * fq) * 8 + fr];
-            a1 = wk[(2 * fq + 1) * 8 + fr];
-          }
+      if (lane < 8) {
+  #pragma unroll
+        for (int p = 0; p < 8; ++p)
+          if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
+        const int kg = k0 + i;  // lane i records pivot i
+        double pv = piv[0];
+  #pragma unroll
+        for (int p = 1; p < 8; ++p) if (i == p) pv = piv[p];
+        dpiv[kg] = pv;
+        dinv[kg] = fast_rcp(pv);
+        const unsigned kind = (kinds >> (2 * i)) & 3u;
+        if (kg < n) {
+          if (dep_att) dep_att[kg] = kind == 1;
+          if (kind == 1) s_dep = 1;
+          if (kind == 2) s_fail = 1;
         }
-        // B[k][c] = P_cK[c][k] (S tiles) or L_cK[c][k] (W tiles), c = Tc*8 + fr
-        const int cc = Tc * 8 + fr;
-        double b0 = M[cc + (k0 + 2 * fq) * CB_LD], b1 = M[cc + (k0 + 2 * fq + 1) * CB_LD];
-        if (t >= n_s) { b0 *= dv0; b1 *= dv1; }
+      }
+      if (lane < 8) {
+  #pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          wk[i * 8 + t] = w[t];
+          if (t < i) M[(k0 + t) + (k0 + i) * CB_LD] = w[t];  // W_{k0+i, k0+t} in the upper part
+        }
+      }
+    };
+    if (warp == 0) phase1(0, wkk[0]);
+
+    __syncthreads();
+    for (int kb = 0; kb < nt; ++kb) {
+      const int k0 = kb * 8;
+      const double *wk = wkk[kb & 1];
+      // ---- phase 2: M[T, K] <- M[T, K] W_KK^T for every row tile T != K
+      for (int T = warp; T < nt; T += nwarps) {
+        if (T == kb) continue;
+        const int r = T * 8 + fr;
+        const double a0 = M[r + (k0 + 2 * fq) * CB_LD], a1 = M[r + (k0 + 2 * fq + 1) * CB_LD];
+        const double b0 = wk[fr * 8 + 2 * fq], b1 = wk[fr * 8 + 2 * fq + 1];  // B[k][j] = W_KK[j][k], j = fr
         double c0 = 0.0, c1 = 0.0;
         dmma8(c0, c1, a0, b0);
         dmma8(c0, c1, a1, b1);
-        const int orow = Tr * 8 + fr, ocol = Tc * 8 + 2 * fq;
-        if (t >= n_s || Tr != Tc || orow >= ocol) M[orow + ocol * CB_LD] -= c0;
-        if (t >= n_s || Tr != Tc || orow >= ocol + 1) M[orow + (ocol + 1) * CB_LD] -= c1;
-      };
-      if (warp == 0) {
-        tile(0);
         __syncwarp();
-        if (tid == 0) stamp(6 + 4 * kb);
-        phase1(kb + 1, wkk[(kb + 1) & 1]);
-        if (tid == 0) stamp(7 + 4 * kb);
-      } else {
-        for (int t = warp; t < n_s + n_w; t += nwarps - 1) tile(t);
-        if (tid == 32) stamp(3);
+        M[r + (k0 + 2 * fq) * CB_LD] = c0;
+        M[r + (k0 + 2 * fq + 1) * CB_LD] = c1;
       }
+      __syncthreads();
+      // ---- phase 3: trailing column tiles Tc > kb.  S part: tiles (Tr >= Tc); W part: Tr <= kb.
+      //      Tile 0 is the next diagonal block: warp 0 updates it and then runs phase 1 of block
+      //      kb + 1 (lookahead) while warps 1.. do the remaining tiles.
+      const int ntrail = nt - kb - 1;
+      if (ntrail > 0) {
+        const int n_s = ntrail * (ntrail + 1) / 2, n_w = (kb + 1) * ntrail;
+        const double dv0 = dinv[k0 + 2 * fq], dv1 = dinv[k0 + 2 * fq + 1];
+        auto tile = [&](int t) {
+          int Tr, Tc;
+          double a0, a1;
+          if (t < n_s) {  // S tile: enumerate (Tr, Tc) with kb < Tc <= Tr
+            int u = t, cnum = 0;
+            while (u >= ntrail - cnum) { u -= ntrail - cnum; ++cnum; }
+            Tc = kb + 1 + cnum;
+            Tr = Tc + u;
+            const int r = Tr * 8 + fr;
+            a0 = M[r + (k0 + 2 * fq) * CB_LD] * dv0;  // L_rK = P_rK Δ^-1
+            a1 = M[r + (k0 + 2 * fq + 1) * CB_LD] * dv1;
+          } else {        // W tile: rows Tr <= kb, A[t][k] = W_{k0+k, t}
+            const int u = t - n_s;
+            Tr = u % (kb + 1);
+            Tc = kb + 1 + u / (kb + 1);
+            const int tr = Tr * 8 + fr;
+            if (Tr < kb) {
+              a0 = M[tr + (k0 + 2 * fq) * CB_LD];
+              a1 = M[tr + (k0 + 2 * fq + 1) * CB_LD];
+            } else {
+              a0 = wk[(2 * fq) * 8 + fr];
+              a1 = wk[(2 * fq + 1) * 8 + fr];
+            }
+          }
+          // B[k][c] = P_cK[c][k] (S tiles) or L_cK[c][k] (W tiles), c = Tc*8 + fr
+          const int cc = Tc * 8 + fr;
+          double b0 = M[cc + (k0 + 2 * fq) * CB_LD], b1 = M[cc + (k0 + 2 * fq + 1) * CB_LD];
+          if (t >= n_s) { b0 *= dv0; b1 *= dv1; }
+          double c0 = 0.0, c1 = 0.0;
+          dmma8(c0, c1, a0, b0);
+          dmma8(c0, c1, a1, b1);
+          const int orow = Tr * 8 + fr, ocol = Tc * 8 + 2 * fq;
+          if (t >= n_s || Tr != Tc || orow >= ocol) M[orow + ocol * CB_LD] -= c0;
+          if (t >= n_s || Tr != Tc || orow >= ocol + 1) M[orow + (ocol + 1) * CB_LD] -= c1;
+        };
+        if (warp == 0) {
+          tile(0);
+          __syncwarp();
+          phase1(kb + 1, wkk[(kb + 1) & 1]);
+        } else {
+          for (int t = warp; t < n_s + n_w; t += nwarps - 1) tile(t);
+        }
+      }
+      __syncthreads();
     }
+    // breakdown with a shift length given: redo on G + s I, s = 11 (m n + n (n+1)) u tr(G)
+    __syncthreads();
+    if (attempt > 0 || !s_fail || !(shift_m > 0.0)) break;
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += G[i + (int64_t)i * ldg];
+    double shift = 11.0 * (shift_m * n + (double)n * (n + 1)) * 0x1p-53 * tr;
+    if (!(shift > 0.0)) shift = 1.0;  // zero matrix: any positive shift
+    __syncthreads();
+    if (tid == 0) {
+      s_fail = 0;
+      atomicOr(flag_word, (unsigned)RQLP_FLAG_SHIFTED_CHOLQR);
+      atomicOr(shift_word, shift_bit);
+    }
+    dep_att = nullptr;
+    load(shift);
     __syncthreads();
   }
   for (int i = tid; i < n; i += blockDim.x) sq[i] = sqrt(dpiv[i]);
@@ -353,7 +379,8 @@ __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsign
 
 void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
-                     const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0) {
+                     const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0, int near_id = 0,
+                     double shift_m = 0.0, unsigned shift_bit = 0) {
   static bool attr = false;
   if (!attr) {
     RQLP_CUDA(cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -362,7 +389,7 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
   }
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
-      c.trace);
+      near_id, shift_m, c.dflags + COND_WORD, shift_bit);
   RQLP_LAUNCHED(c);
 }
 
@@ -437,26 +464,31 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   const unsigned dep_bit = pass_bit << 16;
   gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask);
   if (sharded) allreduce_sum(c, s.G, lc * n);   // Gram summed over the row shards
-  if (second) {
-    // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
-    near_identity_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G, lc, Rout, lc, s.Rinv, lc, condw, pass_bit << 24,
-                                                   cond, mask);
+  if (n <= CHOL_SMALL) {
+    // one kernel: near-identity factor (second pass), else Cholesky + inverse, and on breakdown
+    // the shifted retry in place (marks pass_bit << 8 for the third pass)
+    launch_chol_inv(c, (int)n, s.G, lc, s.G, lc, Rout, lc, s.Rinv, lc, condw, 0u, cond, mask, s.dep, dep_bit,
+                    second ? 1 : 0, (double)m, pass_bit << 8);
+  } else {
+    if (second) {
+      // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
+      near_identity_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G, lc, Rout, lc, s.Rinv, lc, condw, pass_bit << 24,
+                                                     cond, mask);
+      RQLP_LAUNCHED(c);
+      cond = condw;
+      mask = pass_bit << 24;
+    }
+    launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);  // blocked path destroys G
+    chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
+             s.partial_elems, s.dep, dep_bit);
+    // breakdown (ill-conditioned) -> shifted Gram, second attempt (only if pass_bit was set)
+    add_shift_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G2, lc, (double)m, c.dflags + FLAG_WORD, condw, pass_bit,
+                                               pass_bit << 8);
     RQLP_LAUNCHED(c);
-    cond = condw;
-    mask = pass_bit << 24;
+    launch_copy(c, n, n, s.G2, lc, s.G, lc, false, condw, pass_bit);
+    chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
+             s.partial_elems, nullptr, 0u);
   }
-  if (n > CHOL_SMALL) launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);  // blocked path destroys G
-  const double *Gorig = n > CHOL_SMALL ? s.G2 : s.G;
-  chol_inv(c, n, s.G, lc, Gorig, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
-           s.partial_elems, s.dep, dep_bit);
-  // breakdown (ill-conditioned) -> shifted Gram, second attempt (only if pass_bit was set)
-  if (n <= CHOL_SMALL) launch_copy(c, n, n, s.G, lc, s.G2, lc, false, condw, pass_bit);
-  add_shift_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G2, lc, (double)m, c.dflags + FLAG_WORD, condw, pass_bit,
-                                             pass_bit << 8);
-  RQLP_LAUNCHED(c);
-  launch_copy(c, n, n, s.G2, lc, s.G, lc, false, condw, pass_bit);
-  chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
-           s.partial_elems, nullptr, 0u);
   gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, gcond, gmask);
   // rank-deficient columns -> random completion, orthonormalised by the following pass
   replace_dep_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
