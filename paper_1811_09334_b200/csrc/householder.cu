@@ -112,12 +112,15 @@ __device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
 // meet at the step's single __syncthreads; every warp then reduces the 32 slots itself.
 template <bool GRID, bool SMEMC>
 __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs a) {
-  extern __shared__ double smem[];
-  double *vraw = smem;
-  double *vn1 = vraw + a.rows;
-  double *rvn2 = vn1 + a.owned_max;  // 1 / (squared norm at the last recompute)
-  double *colbuf = rvn2 + a.owned_max;
-  int *done_l = reinterpret_cast<int *>(colbuf + (SMEMC ? (int64_t)a.owned_max * a.rows : 0));
+  extern __shared__ __align__(16) double smem[];
+  // even strides keep every cached column and the pivot column 16-byte aligned (double2 access
+  // in absolute row coordinates); the padding row is zero and stays zero
+  const int rs = (a.rows + 1) & ~1, op = (a.owned_max + 1) & ~1;
+  double *vraw = smem;                   // pivot column rows j.. at their absolute positions
+  double *vn1 = vraw + rs;
+  double *rvn2 = vn1 + op;               // 1 / (squared norm at the last recompute)
+  double *colbuf = rvn2 + op;
+  int *done_l = reinterpret_cast<int *>(colbuf + (SMEMC ? (int64_t)a.owned_max * rs : 0));
   __shared__ double s_bv[2][32];
   __shared__ int s_bi[2][32];
   __shared__ int s_p;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   const int nown = b < a.cols ? (a.cols - b + G - 1) / G : 0;  // columns b, b+G, b+2G, ...
   const int rows = a.rows;
   auto colptr = [&](int li) -> double * {
-    if (SMEMC) return colbuf + (int64_t)li * rows;
+    if (SMEMC) return colbuf + (int64_t)li * rs;
     return a.M + (int64_t)(b + li * G) * a.ldm;
   };
   auto cta_best = [&](int par) -> Best {  // every warp: argmax of the 32 warp slots
@@ -161,7 +164,9 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
 
   if (SMEMC)
     for (int li = 0; li < nown; ++li)
-      for (int r = threadIdx.x; r < rows; r += blockDim.x) colbuf[(int64_t)li * rows + r] = a.M[(int64_t)(b + li * G) * a.ldm + r];
+      for (int r = threadIdx.x; r < rs; r += blockDim.x)
+        colbuf[(int64_t)li * rs + r] = r < rows ? a.M[(int64_t)(b + li * G) * a.ldm + r] : 0.0;
+  if (threadIdx.x == 0 && rs > rows) vraw[rows] = 0.0;
   for (int li = threadIdx.x; li < nown; li += blockDim.x) {
     done_l[li] = 0;
     a.done[b + li * G] = 0;
@@ -185,9 +190,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
     const int par = j & 1;
     auto stamp = [&](int ph) {
       if (a.trace && b == 0 && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.trace[(int64_t)j * 4 + ph] = t;
+        a.trace[(int64_t)j * 4 + ph] = (unsigned long long)clock64();  // SM cycles
       }
     };
     stamp(0);
@@ -240,10 +243,10 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
           lo = src[2 * r];
           hi = src[2 * r + 1];
         } while ((unsigned)lo != tag || (unsigned)hi != tag);
-        vraw[r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
+        vraw[j + r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
       }
       __syncthreads();
-      cp = vraw;
+      cp = vraw + j;
     } else {
       p = a.pivot ? cta_best(par).i : j;
       cp = colptr(p) + j;
@@ -298,21 +301,56 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
         double *col = colptr(li) + j;
         double x = col[0];
         if (tau != 0.0) {
-          double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;  // two chains of the dot product
-          int r = 1 + l8;
-          for (; r + 8 < len; r += 16) {
-            w0 = fma(cp[r] * scal, col[r], w0);
-            w1 = fma(cp[r + 8] * scal, col[r + 8], w1);
+          if (SMEMC) {
+            // absolute rows: the odd leading row j+1 (if any) by lane 0, then aligned pairs
+            const double *cpa = cp - j;
+            double *cab = col - j;
+            const int a0 = (j + 2) & ~1;
+            double d0 = 0.0, d1 = 0.0;
+            if (l8 == 0 && j + 1 < a0 && j + 1 < rows) d0 = cpa[j + 1] * cab[j + 1];
+#pragma unroll 2
+            for (int ar = a0 + 2 * l8; ar < rows; ar += 16) {
+              const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
+              const double2 u = *reinterpret_cast<const double2 *>(cab + ar);
+              d0 = fma(v.x, u.x, d0);
+              d1 = fma(v.y, u.y, d1);
+            }
+            double dot = d0 + d1;
+            dot += __shfl_xor_sync(gmask, dot, 4);
+            dot += __shfl_xor_sync(gmask, dot, 2);
+            dot += __shfl_xor_sync(gmask, dot, 1);
+            const double w = tau * fma(scal, dot, x);   // tau v^T col, v = [1; cp[1..] scal]
+            const double ws = w * scal;
+            x -= w;  // the updated row-j entry (identical in the 8 lanes)
+            if (l8 == 0) {
+              col[0] = x;
+              if (j + 1 < a0 && j + 1 < rows) cab[j + 1] = fma(-ws, cpa[j + 1], cab[j + 1]);
+            }
+#pragma unroll 2
+            for (int ar = a0 + 2 * l8; ar < rows; ar += 16) {
+              const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
+              double2 u = *reinterpret_cast<const double2 *>(cab + ar);
+              u.x = fma(-ws, v.x, u.x);
+              u.y = fma(-ws, v.y, u.y);
+              *reinterpret_cast<double2 *>(cab + ar) = u;
+            }
+          } else {
+            double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;  // two chains of the dot product
+            int r = 1 + l8;
+            for (; r + 8 < len; r += 16) {
+              w0 = fma(cp[r] * scal, col[r], w0);
+              w1 = fma(cp[r + 8] * scal, col[r + 8], w1);
+            }
+            if (r < len) w0 = fma(cp[r] * scal, col[r], w0);
+            double w = w0 + w1;
+            w += __shfl_xor_sync(gmask, w, 4);
+            w += __shfl_xor_sync(gmask, w, 2);
+            w += __shfl_xor_sync(gmask, w, 1);
+            w *= tau;
+            x -= w;  // the updated row-j entry (identical in the 8 lanes)
+            if (l8 == 0) col[0] = x;
+            for (int rr = 1 + l8; rr < len; rr += 8) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
           }
-          if (r < len) w0 = fma(cp[r] * scal, col[r], w0);
-          double w = w0 + w1;
-          w += __shfl_xor_sync(gmask, w, 4);
-          w += __shfl_xor_sync(gmask, w, 2);
-          w += __shfl_xor_sync(gmask, w, 1);
-          w *= tau;
-          x -= w;  // the updated row-j entry (identical in the 8 lanes)
-          if (l8 == 0) col[0] = x;
-          for (int rr = 1 + l8; rr < len; rr += 8) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
           __syncwarp(gmask);
         }
         if (a.pivot) {
@@ -351,7 +389,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   __syncthreads();
   if (SMEMC)
     for (int li = 0; li < nown; ++li)
-      for (int r = threadIdx.x; r < rows; r += blockDim.x) a.M[(int64_t)(b + li * G) * a.ldm + r] = colbuf[(int64_t)li * rows + r];
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) a.M[(int64_t)(b + li * G) * a.ldm + r] = colbuf[(int64_t)li * rs + r];
 }
 
 // perm[steps..cols) = not-pivoted columns in ascending original order (single CTA scan).
@@ -483,13 +521,19 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
   a.epoch = 0;
   a.trace = c.trace;
   auto smem_for = [&](int64_t owned, bool cached) {
-    return (size_t)(rows + 2 * owned + (cached ? owned * rows : 0)) * 8 + (size_t)owned * 4 + 64;
+    const int64_t rs = round_up(rows, 2), op = round_up(owned, 2);
+    return (size_t)(rs + 2 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;
   };
   if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
     // whole matrix in one CTA's shared memory: no global exchange at all
     a.owned_max = (int)cols;
     set_engine_attr<false, true>();
-    hh_engine_kernel<false, true><<<1, 1024, smem_for(cols, true), c.stream>>>(a);
+    static int single_threads = -1;
+    if (single_threads < 0) {
+      const char *e = getenv("RQLP_ENGINE_T1");
+      single_threads = e ? atoi(e) : 1024;
+    }
+    hh_engine_kernel<false, true><<<1, single_threads, smem_for(cols, true), c.stream>>>(a);
     RQLP_LAUNCHED(c);
   } else {
     // enough CTAs that each owns >= 8 columns (fewer records to exchange), at most one per SM
@@ -513,7 +557,12 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     // through cudaLaunchKernelEx (capturable into CUDA graphs)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(512);
+    static int grid_threads = -1;
+    if (grid_threads < 0) {
+      const char *e = getenv("RQLP_ENGINE_TG");
+      grid_threads = e ? atoi(e) : 512;
+    }
+    cfg.blockDim = dim3((unsigned)grid_threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
