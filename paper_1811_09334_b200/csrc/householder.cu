@@ -284,9 +284,17 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
     //      8-lane groups: a warp updates 4 columns at once (3-step group reductions).
     best = Best{-1.0, 0x7fffffff};
     {
-      const int g8 = lane >> 3, l8 = lane & 7;
-      const unsigned gmask = 0xffu << (8 * g8);
-      for (int li = warp * 4 + g8; li < nown; li += wpb * 4) {
+      // column groups: 8 lanes per column for shared-memory columns (a warp updates 4 at once),
+      // a whole warp per column for columns in global memory (more loads in flight per column)
+      constexpr int GS = SMEMC ? 8 : 32, GPW = 32 / GS;
+      const int g8 = lane / GS, l8 = lane % GS;
+      const unsigned gmask = GS == 32 ? 0xffffffffu : (0xffu << (8 * g8));
+      auto gsum = [&](double v) {
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+        return v;
+      };
+      for (int li = warp * GPW + g8; li < nown; li += wpb * GPW) {
         const int gi = b + li * G;
         if (gi == p || done_l[li]) continue;
         // downdating operands first (off the dependency chain): 1/vn1 and vn1/vn2 (rvn2 = 1/vn2)
@@ -315,10 +323,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
               d0 = fma(v.x, u.x, d0);
               d1 = fma(v.y, u.y, d1);
             }
-            double dot = d0 + d1;
-            dot += __shfl_xor_sync(gmask, dot, 4);
-            dot += __shfl_xor_sync(gmask, dot, 2);
-            dot += __shfl_xor_sync(gmask, dot, 1);
+            const double dot = gsum(d0 + d1);
             const double w = tau * fma(scal, dot, x);   // tau v^T col, v = [1; cp[1..] scal]
             const double ws = w * scal;
             x -= w;  // the updated row-j entry (identical in the 8 lanes)
@@ -335,21 +340,17 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
               *reinterpret_cast<double2 *>(cab + ar) = u;
             }
           } else {
-            double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;  // two chains of the dot product
-            int r = 1 + l8;
-            for (; r + 8 < len; r += 16) {
-              w0 = fma(cp[r] * scal, col[r], w0);
-              w1 = fma(cp[r + 8] * scal, col[r + 8], w1);
-            }
-            if (r < len) w0 = fma(cp[r] * scal, col[r], w0);
-            double w = w0 + w1;
-            w += __shfl_xor_sync(gmask, w, 4);
-            w += __shfl_xor_sync(gmask, w, 2);
-            w += __shfl_xor_sync(gmask, w, 1);
+            // columns in global memory (L2): a simple strided loop the compiler unrolls, so many
+            // loads are in flight
+            double w = l8 == 0 ? x : 0.0;
+#pragma unroll 8
+            for (int r = 1 + l8; r < len; r += GS) w = fma(cp[r] * scal, col[r], w);
+            w = gsum(w);
             w *= tau;
             x -= w;  // the updated row-j entry (identical in the 8 lanes)
             if (l8 == 0) col[0] = x;
-            for (int rr = 1 + l8; rr < len; rr += 8) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
+#pragma unroll 8
+            for (int rr = 1 + l8; rr < len; rr += GS) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
           }
           __syncwarp(gmask);
         }
@@ -362,10 +363,8 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
             const double t2 = t * q12;
             if (t2 <= TOL3Z) {
               double ss = 0.0;
-              for (int rr = 1 + l8; rr < len; rr += 8) ss = fma(col[rr], col[rr], ss);
-              ss += __shfl_xor_sync(gmask, ss, 4);
-              ss += __shfl_xor_sync(gmask, ss, 2);
-              ss += __shfl_xor_sync(gmask, ss, 1);
+              for (int rr = 1 + l8; rr < len; rr += GS) ss = fma(col[rr], col[rr], ss);
+              ss = gsum(ss);
               n1 = (j + 1 < rows) ? ss : 0.0;
               if (l8 == 0) rvn2[li] = n1 != 0.0 ? 1.0 / n1 : 0.0;
             } else {
