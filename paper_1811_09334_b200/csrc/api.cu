@@ -411,6 +411,33 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
+  // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
+  auto reorth = [&](int64_t c0, int64_t bj) {
+    if (c0 == 0) return;
+    double *Vj = P.V + c0 * ldm;
+    c.mark("b_other");
+    gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
+    allreduce_sum(c, P.C, LL * bj);
+    gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
+                    nullptr, 0);
+    launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
+    orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
+  };
+  // q = 0 (NEXT-4): the range finder needs no A-pass per block, so every V_j is built first
+  // and ONE batched pass B = V^T A replaces the h per-block projections; the deflation
+  // B_j = V_j^T A - (V_j^T V_<j) B_<j below is unchanged (exact-arithmetic identity).
+  const bool two_pass = q == 0 && !ar;
+  if (two_pass) {
+    for (int64_t j = 0; j < h_blocks; ++j) {
+      const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
+      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, P.V + c0 * ldm, ldm, nullptr, 0, sh);  // l.4
+      reorth(c0, bj);                                                                       // l.5
+    }
+    c.mark("b_other");
+    gemm_tn(c, m, l, n, A, lda, P.V, ldm, B, LL, true, P.part, P.part_elems);           // all V_j^T A
+    allreduce_sum(c, B, LL * n);
+    c.mark("pass_project");
+  }
   for (int64_t j = 0; j < h_blocks; ++j) {
     const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
     double *Vj = P.V + c0 * ldm;
@@ -419,50 +446,45 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       gemm_nn(c, m, bj, n, A, lda, P.Om + c0 * ldn, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems);
       c.mark("pass_block_sketch");
     }
-    // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
-    auto reorth = [&]() {
-      if (c0 == 0) return;
-      c.mark("b_other");
-      gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
-      allreduce_sum(c, P.C, LL * bj);
-      gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
-                      nullptr, 0);
-      launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
-      orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
-    };
-    orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
-    reorth();                                                                            // l.5
-    for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
-      c.mark("b_other");
-      gemm_tn(c, m, bj, n, A, lda, Vj, ldm, P.Z, ldn, false, P.part, P.part_elems);     // Z = A^T Vj
-      allreduce_sum(c, P.Z, ldn * bj);
-      c.mark("pass_block_AtV");
-      if (c0 > 0) {
-        gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems); // C = V_<j^T Vj
-        allreduce_sum(c, P.C, LL * bj);
-        gemm_generic_ex(c, true, false, n, bj, c0, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems, false,
-                        nullptr, 0);                                                     // Z -= B_<j^T C
+    if (!two_pass) {
+      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
+      reorth(c0, bj);                                                                      // l.5
+      for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
+        c.mark("b_other");
+        gemm_tn(c, m, bj, n, A, lda, Vj, ldm, P.Z, ldn, false, P.part, P.part_elems);     // Z = A^T Vj
+        allreduce_sum(c, P.Z, ldn * bj);
+        c.mark("pass_block_AtV");
+        if (c0 > 0) {
+          gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems); // C = V_<j^T Vj
+          allreduce_sum(c, P.C, LL * bj);
+          gemm_generic_ex(c, true, false, n, bj, c0, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems, false,
+                          nullptr, 0);                                                     // Z -= B_<j^T C
+        }
+        orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
+        c.mark("b_other");
+        gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
+        c.mark("pass_block_AW");
+        if (c0 > 0) {
+          gemm_generic_ex(c, false, false, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems, false,
+                          nullptr, 0);                                                     // D = B_<j W
+          gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part,
+                          P.part_elems, false, nullptr, 0);                                // Y -= V_<j D
+        }
+        orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
+        reorth(c0, bj);
       }
-      orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
-      c.mark("b_other");
-      gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
-      c.mark("pass_block_AW");
-      if (c0 > 0) {
-        gemm_generic_ex(c, false, false, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems, false,
-                        nullptr, 0);                                                     // D = B_<j W
-        gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part,
-                        P.part_elems, false, nullptr, 0);                                // Y -= V_<j D
-      }
-      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
-      reorth();
     }
     // l.6: B_j = Vj^T A^(j-1) = Vj^T A - (Vj^T V_<j) B_<j, formed in the tail's B buffer
     double *Bj = P.tail.Bw;
     const int64_t ldbj = P.tail.ldl;
     c.mark("b_other");
-    gemm_tn(c, m, bj, n, A, lda, Vj, ldm, Bj, ldbj, true, P.part, P.part_elems);
-    allreduce_sum(c, Bj, ldbj * n);
-    c.mark("pass_block_project");
+    if (two_pass) {
+      launch_copy(c, bj, n, B + c0, LL, Bj, ldbj, false);   // V_j^T A from the batched pass
+    } else {
+      gemm_tn(c, m, bj, n, A, lda, Vj, ldm, Bj, ldbj, true, P.part, P.part_elems);
+      allreduce_sum(c, Bj, ldbj * n);
+      c.mark("pass_block_project");
+    }
     if (c0 > 0) {
       const int64_t lde = round_up(b, 8);
       gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, lde, false, P.part, P.part_elems);   // E = Vj^T V_<j (bj x c0)

@@ -145,6 +145,8 @@ CASES = [  # (name, m, n, k, p, q, d, sigma)
     ("d1", 700, 500, 40, 8, 0, 1, lambda j: j**-1.5),
     ("d4", 700, 500, 40, 8, 0, 4, lambda j: j**-1.5),
     ("wide", 300, 900, 40, 8, 1, 0, lambda j: j**-1.0),
+    ("d5", 700, 500, 40, 8, 1, 5, lambda j: j**-1.5),      # NEXT-4: larger odd / even d
+    ("d6", 700, 500, 40, 8, 0, 6, lambda j: np.exp(-j / 30.0)),
 ]
 
 
@@ -333,3 +335,21 @@ def test_tqlp_parity(rq, orc, case):
     assert np.abs(Pg.T @ Pg - np.eye(l)).max() <= 1e-13 * l
     assert not np.triu(_np(g["T"]), 1).any()
 
+
+
+def test_brqlp_q0_two_passes(rq, orc):
+    """NEXT-4: BRQLP with q = 0 reads A exactly twice (one batched sketch, one batched
+    projection) instead of 1 + h times, with the same result as the oracle's explicit deflation."""
+    m, n, k, p, b = 1200, 500, 60, 12, 16        # h = 5 blocks, ragged last block
+    A = _rand_svd(m, n, np.exp(-np.arange(1, 501.0) / 60), 314)
+    h = rq.Handle.default()
+    h.set_timing(True)
+    try:
+        g = rq.factorize(_cm(A), k, p, q=0, b=b, seed=9)
+        names = [nm for nm, _ in h.timing()]
+    finally:
+        h.set_timing(False)
+    o = orc.brqlp(A, k, p, b=b, q=0, seed=9)
+    _check_factorization(rq, orc, A, g, o, k + p)
+    passes = [nm for nm in names if nm.startswith("pass_")]
+    assert passes == ["pass_sketch", "pass_project"], passes

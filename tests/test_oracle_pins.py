@@ -449,3 +449,18 @@ def test_tqlp_full_rank_is_exact(orc):
     A = _rand_svd(50, 35, np.logspace(0, -6, 35), 77)
     o = orc.tqlp(A, 35)
     np.testing.assert_allclose(o["Q"] @ o["T"] @ o["P"].T, A, atol=1e-14)
+
+
+def test_erqlp_more_inner_qr_tracks_better(orc):
+    """Theorem 2: more inner QR iterations give L-values closer to the
+    singular values (quadratic improvement per step for gapped spectra).  Max relative L-value
+    error over j <= k for d = 0, 2, 4, 6 on a gapped spectrum, fixed seed."""
+    k, p = 12, 4
+    sig = 0.6 ** np.arange(40.0)
+    A = _rand_svd(120, 40, sig, 55)
+    errs = []
+    for d in (0, 2, 4, 6):
+        out = orc.rqlp(A, k, p, q=1, d=d, seed=3)
+        lv = np.abs(np.diag(out["T"]))[:k]
+        errs.append(np.max(np.abs(lv - sig[:k]) / sig[:k]))
+    assert errs[1] < errs[0] and errs[2] < errs[1] and errs[3] <= errs[2] * 1.01, errs
