@@ -266,9 +266,9 @@ int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap
   const double hbm = 6.0e12;                                           // B/s
   int best = 1;
   double best_t = 1e300;
-  for (int s = 1; s <= 64; ++s) {
+  for (int s = 1; s <= 2 * num_sms; ++s) {
     if (s > 1 && (size_t)s * out_elems > partial_cap_elems) break;
-    if (s > 1 && ktiles / s < 4) break;
+    if (s > 1 && ktiles / s < 2) break;
     const int64_t T = tiles * s;
     double t = (double)ceil_div(T, num_sms) * (double)ceil_div(ktiles, s) * t_ktile;
     if (s > 1) t += 2.0 * s * (double)out_elems * 8.0 / hbm + 4e-6;
