@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   double *vraw = smem;                   // pivot column rows j.. at their absolute positions
   double *vn1 = vraw + rs;
   double *rvn2 = vn1 + op;               // 1 / (squared norm at the last recompute)
-  double *colbuf = rvn2 + op;
+  double *wsbuf = rvn2 + op;             // deferred rank-1 update factors (GRID, cached, pivoted)
+  double *colbuf = wsbuf + op;
   int *done_l = reinterpret_cast<int *>(colbuf + (SMEMC ? (int64_t)a.owned_max * rs : 0));
   __shared__ double s_bv[2][32];
   __shared__ int s_bi[2][32];
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
   const int G = GRID ? (int)gridDim.x : 1, b = GRID ? (int)blockIdx.x : 0;
   const int nown = b < a.cols ? (a.cols - b + G - 1) / G : 0;  // columns b, b+G, b+2G, ...
   const int rows = a.rows;
+  const bool DEFER = GRID && SMEMC && a.pivot;
   auto colptr = [&](int li) -> double * {
     if (SMEMC) return colbuf + (int64_t)li * rs;
     return a.M + (int64_t)(b + li * G) * a.ldm;
@@ -327,17 +329,21 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
             const double w = tau * fma(scal, dot, x);   // tau v^T col, v = [1; cp[1..] scal]
             const double ws = w * scal;
             x -= w;  // the updated row-j entry (identical in the 8 lanes)
-            if (l8 == 0) {
-              col[0] = x;
-              if (j + 1 < a0 && j + 1 < rows) cab[j + 1] = fma(-ws, cpa[j + 1], cab[j + 1]);
-            }
+            if (l8 == 0) col[0] = x;
+            if (DEFER) {
+              // rows j+1.. are updated after the publish (off the exchange's critical path);
+              // the downdate below needs only the row-j entry
+              if (l8 == 0) wsbuf[li] = ws;
+            } else {
+              if (l8 == 0 && j + 1 < a0 && j + 1 < rows) cab[j + 1] = fma(-ws, cpa[j + 1], cab[j + 1]);
 #pragma unroll 2
-            for (int ar = a0 + 2 * l8; ar < rows; ar += 16) {
-              const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
-              double2 u = *reinterpret_cast<const double2 *>(cab + ar);
-              u.x = fma(-ws, v.x, u.x);
-              u.y = fma(-ws, v.y, u.y);
-              *reinterpret_cast<double2 *>(cab + ar) = u;
+              for (int ar = a0 + 2 * l8; ar < rows; ar += 16) {
+                const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
+                double2 u = *reinterpret_cast<const double2 *>(cab + ar);
+                u.x = fma(-ws, v.x, u.x);
+                u.y = fma(-ws, v.y, u.y);
+                *reinterpret_cast<double2 *>(cab + ar) = u;
+              }
             }
           } else {
             // columns in global memory (L2): a simple strided loop the compiler unrolls, so many
@@ -362,6 +368,13 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
             t = t < 0.0 ? 0.0 : t;
             const double t2 = t * q12;
             if (t2 <= TOL3Z) {
+              if (DEFER && tau != 0.0) {  // the recomputed norm needs the updated rows now
+                __syncwarp(gmask);
+                const double ws = wsbuf[li];
+                for (int rr = 1 + l8; rr < len; rr += GS) col[rr] = fma(-ws, cp[rr], col[rr]);
+                __syncwarp(gmask);
+                if (l8 == 0) wsbuf[li] = 0.0;
+              }
               double ss = 0.0;
               for (int rr = 1 + l8; rr < len; rr += GS) ss = fma(col[rr], col[rr], ss);
               ss = gsum(ss);
@@ -383,7 +396,30 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
     }
     __syncthreads();
     stamp(3);
-    if (GRID && warp == 0 && j + 1 < a.steps) publish(j + 1, cta_best(par ^ 1));
+    if (DEFER) {
+      // every warp derives the CTA's candidate; warp 0 completes its update and publishes it,
+      // then all groups complete the other columns (before the next step's fetch barrier)
+      const Best cb = cta_best(par ^ 1);
+      const int lbest = cb.i != 0x7fffffff ? (cb.i - b) / G : -1;
+      auto finish = [&](int li, int l0, int stride) {
+        const double ws = wsbuf[li];
+        if (ws == 0.0) return;
+        double *cab = colptr(li);
+        for (int r = j + 1 + l0; r < rows; r += stride) cab[r] = fma(-ws, cp[r - j], cab[r]);
+      };
+      if (warp == 0) {
+        if (lbest >= 0 && tau != 0.0) finish(lbest, lane, 32);
+        __syncwarp();
+        if (j + 1 < a.steps) publish(j + 1, cb);
+      }
+      if (tau != 0.0) {
+        const int g8 = lane >> 3, l8 = lane & 7;
+        for (int li = warp * 4 + g8; li < nown; li += wpb * 4)
+          if (li != lbest && b + li * G != p && !done_l[li]) finish(li, l8, 8);
+      }
+    } else if (GRID && warp == 0 && j + 1 < a.steps) {
+      publish(j + 1, cta_best(par ^ 1));
+    }
   }
   __syncthreads();
   if (SMEMC)
@@ -521,7 +557,7 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
   a.trace = c.trace;
   auto smem_for = [&](int64_t owned, bool cached) {
     const int64_t rs = round_up(rows, 2), op = round_up(owned, 2);
-    return (size_t)(rs + 2 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;
+    return (size_t)(rs + 3 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;
   };
   if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
     // whole matrix in one CTA's shared memory: no global exchange at all
