@@ -504,7 +504,6 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       ar->err = ar->a2 > 0.0 ? std::sqrt(e2 > 0.0 ? e2 : 0.0) / std::sqrt(ar->a2) : 0.0;
       ar->l_out = (int)(c0 + bj);
       stop = e2 <= ar->eps * ar->eps * ar->a2;
-      if (getenv("RQLP_AR_DEBUG")) fprintf(stderr, "[autorank] block %lld a2 %.17g b2 %.17g\n", (long long)j, ar->a2, b2);
     }
     // l.8: [Q_B, L_j, P_B] = qlp(B_j) (overwrites the tail's copy)
     qlp_tail(c, P.tail, bj, n, P.tail.Bw, P.tail.ldl, 0, P.QB, P.tail.ldl, L + c0 + c0 * ldl, ldl, Pout + c0 * ldp,
