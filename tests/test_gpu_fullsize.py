@@ -113,8 +113,17 @@ def _staged(rq, orc, c, A, g, n_rows=256, tail_d=None):
     Y_g = _np(g["Y"][idx, :])
     bound = 64 * U * n * (np.abs(A_s) @ np.abs(Om_o))
     assert np.all(np.abs(Y_g - Y_o) <= bound)
-    # 3. the oracle's tail on the GPU's B: pivots, L-values, T, Q_B, P_B
+    # 3. sampled columns of the projection pass B = V^T A (RQLP/ERQLP: B is exactly V^T A;
+    #    BRQLP's B_j carries the deflation terms, checked through eq. (21) by the callers)
     B = _np(g["B"])
+    if c.b is None:
+        cols = np.sort(rng.choice(n, size=32, replace=False))
+        cidx = torch.from_numpy(cols).to(A.device)
+        V_h, A_c = _np(g["V"]), _np(A[:, cidx])
+        B_o = orc.gemm_tn(V_h, A_c)
+        bound = 64 * U * m * (np.abs(V_h).T @ np.abs(A_c))
+        assert np.all(np.abs(B[:, cols] - B_o) <= bound)
+    # 4. (callers) the oracle's tail on the GPU's B: pivots, L-values, T, Q_B, P_B
     return B
 
 
