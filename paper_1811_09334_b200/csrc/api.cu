@@ -50,6 +50,18 @@ struct rqlp_handle_s {
 
 namespace rqlpk {
 
+void smem_attr(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, int> done;
+  int dev = 0;
+  RQLP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  int &have = done[{dev, kernel}];
+  if (have >= bytes) return;
+  RQLP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
 void launch_reduce(Ctx &c, int64_t M, int64_t N, int S, const double *part, double alpha, double beta, double *C,
                    int64_t ldc, bool trans, const unsigned *cond, unsigned cond_mask);
 void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,

@@ -285,11 +285,7 @@ void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int 
                int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask) {
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
-  static bool attr = false;
-  if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(gemm_tma_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
-  }
+  smem_attr((const void *)gemm_tma_kernel<BN, MODE>, SMEM);
   int kps = (int)ceil_div(ktiles, S);
   S = (int)ceil_div(ktiles, kps);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);

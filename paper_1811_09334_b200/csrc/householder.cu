@@ -519,12 +519,7 @@ void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms, i
 
 template <bool GRID, bool SMEMC>
 static void set_engine_attr() {
-  static bool done = false;
-  if (!done) {
-    RQLP_CUDA(cudaFuncSetAttribute(hh_engine_kernel<GRID, SMEMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   220 * 1024));
-    done = true;
-  }
+  smem_attr((const void *)hh_engine_kernel<GRID, SMEMC>, 220 * 1024);
 }
 
 void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int64_t ldm, bool pivot, int64_t steps) {
@@ -609,12 +604,8 @@ void hh_form_q(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *Q, int6
   const bool qsmem = (size_t)rows * 8 <= 200 * 1024;
   if (!qsmem) nw = 8;
   const size_t qbytes = qsmem ? (size_t)nw * rows * 8 : 0;
-  static bool attr = false;
-  if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    RQLP_CUDA(cudaFuncSetAttribute(form_q_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr((const void *)form_q_kernel<true, true>, 200 * 1024);
+  smem_attr((const void *)form_q_kernel<false, true>, 200 * 1024);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(steps, nw), (int64_t)c.num_sms));
   if (qsmem && vbytes + qbytes <= 190 * 1024) {
     form_q_kernel<true, true><<<grid, nw * 32, vbytes + qbytes, c.stream>>>((int)rows, (int)steps, s.Vst, s.tau,

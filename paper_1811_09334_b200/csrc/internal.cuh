@@ -47,6 +47,10 @@ static inline bool sync_debug() {
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Raise a kernel's dynamic shared-memory limit once per (device, kernel): the attribute is per
+// device and one process may drive several devices (defined in api.cu).
+void smem_attr(const void *kernel, int bytes);
+
 #ifdef __CUDACC__
 // 1/x and sqrt(x) to ~1 ulp without the IEEE routines' slow-path branches: MUFU seed + Newton
 // steps (x positive and normal; callers handle zero / non-finite values before).

@@ -381,12 +381,7 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
                      const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0, int near_id = 0,
                      double shift_m = 0.0, unsigned shift_bit = 0) {
-  static bool attr = false;
-  if (!attr) {
-    RQLP_CUDA(cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CHOL_SMALL * CB_LD * 8));
-    attr = true;
-  }
+  smem_attr((const void *)chol_blk_kernel, CHOL_SMALL * CB_LD * 8);
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
       near_id, shift_m, c.dflags + COND_WORD, shift_bit);
