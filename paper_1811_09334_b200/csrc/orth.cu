@@ -74,12 +74,54 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   __shared__ int s_fail, s_dep;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int npad = (n + 7) & ~7, nt = npad >> 3;
+  // M(b, a) = G[a + b ldg] (+ shift on the diagonal) for a <= b: the lower part (read coalesced
+  // over a; a flat unrolled loop keeps many loads in flight -- one CTA streams the whole matrix),
+  // the upper part (the W^T entries) zero, identity padding.  shift > 0: the retry after a
+  // breakdown (shifted CholeskyQR, G + shift I); dep detection is then off.
+  auto load = [&](double shift) {
+    // row pairs (a, a+1) of column b: 16-byte loads when the column start is 16-byte aligned
+    const int hp = npad >> 1, tot = hp * npad;
+    const bool vec = ((ldg & 1) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
+    // (pair index, column) advanced incrementally: no integer division in the loop
+    const int da = blockDim.x % hp, db = blockDim.x / hp;
+    int ai = tid % hp, bi = tid / hp;
+#pragma unroll 8
+    for (int e = tid; e < tot; e += blockDim.x) {
+      const int a = 2 * ai, b = bi;
+      ai += da;
+      bi += db;
+      if (ai >= hp) { ai -= hp; ++bi; }
+      if (a > b) continue;
+      double v0 = (a == b) ? 1.0 : 0.0, v1 = (a + 1 == b) ? 1.0 : 0.0;
+      if (b < n) {
+        const double *src = G + a + (int64_t)b * ldg;  // a + 1 <= npad - 1; rows >= n are unused
+        if (vec && a + 1 < n) {
+          const double2 t = *reinterpret_cast<const double2 *>(src);
+          v0 = t.x; v1 = t.y;
+        } else {
+          v0 = src[0];
+          v1 = a + 1 < n ? src[1] : v1;
+        }
+        if (a == b) v0 += shift;
+        if (a + 1 == b) v1 += shift;
+      }
+      M[b + a * CB_LD] = v0;
+      if (a < b) M[a + b * CB_LD] = 0.0;
+      if (a + 1 <= b) {
+        M[b + (a + 1) * CB_LD] = v1;
+        if (a + 1 < b) M[a + 1 + b * CB_LD] = 0.0;
+      }
+    }
+    for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
+  };
+  load(0.0);
+  __syncthreads();
   if (near_id) {
     // CholeskyQR2's second pass: if max |G - I| <= 2^-27, R = I + triu(E,1) + diag(E)/2 and
     // X = I - (same) are exact to below u (the neglected terms are O(|E|^2))
     double emax = 0.0;
     for (int b = warp; b < n; b += nwarps)
-      for (int a = lane; a < n; a += 32) emax = fmax(emax, fabs(G[a + (int64_t)b * ldg] - (a == b ? 1.0 : 0.0)));
+      for (int a = lane; a <= b; a += 32) emax = fmax(emax, fabs(M[b + a * CB_LD] - (a == b ? 1.0 : 0.0)));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
     if (lane == 0) red[warp] = emax;
@@ -88,32 +130,16 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
     for (int w = 0; w < nwarps; ++w) mx = fmax(mx, red[w]);
     if (mx <= 0x1p-27) {
       for (int b = warp; b < n; b += nwarps)
-        for (int a = lane; a < n; a += 32) {
-          const double g = G[a + (int64_t)b * ldg];
+        for (int a = lane; a < n; a += 32) {  // (a, b) of R and X, coalesced over a
           double u = 0.0;
-          if (a < b) u = g;
-          else if (a == b) u = 0.5 * (g - 1.0);
+          if (a < b) u = M[b + a * CB_LD];
+          else if (a == b) u = 0.5 * (M[a + a * CB_LD] - 1.0);
           R[a + (int64_t)b * ldr] = (a == b ? 1.0 : 0.0) + u;
           X[a + (int64_t)b * ldx] = (a == b ? 1.0 : 0.0) - u;
         }
       return;
     }
   }
-  // shift > 0: the retry after a breakdown (shifted CholeskyQR, G + shift I); dep detection off
-  auto load = [&](double shift) {
-    // M(b, a) = G[a + b ldg] for a <= b (the lower part, read coalesced over a), the upper part
-    // (the W^T entries) zero, identity padding
-    for (int b = warp; b < npad; b += nwarps)
-      for (int a = lane; a < npad; a += 32) {
-        double v = 0.0;
-        if (a < n && b < n) { if (a <= b) v = G[a + (int64_t)b * ldg] + (a == b ? shift : 0.0); }
-        else if (a == b) v = 1.0;
-        M[b + a * CB_LD] = v;
-        if (a < b) M[a + b * CB_LD] = 0.0;
-      }
-    for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
-  };
-  load(0.0);
   if (tid == 0) { s_fail = 0; s_dep = 0; }
   __syncthreads();
   int *dep_att = dep;
@@ -250,7 +276,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
     __syncthreads();
     if (attempt > 0 || !s_fail || !(shift_m > 0.0)) break;
     double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += G[i + (int64_t)i * ldg];
+    for (int i = 0; i < n; ++i) tr += g0s[i];  // = diag(G): the fused path has Gorig == G
     double shift = 11.0 * (shift_m * n + (double)n * (n + 1)) * 0x1p-53 * tr;
     if (!(shift > 0.0)) shift = 1.0;  // zero matrix: any positive shift
     __syncthreads();
