@@ -533,8 +533,7 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
   cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded, true);
   if (R) {  // R = R2 R1
-    gemm_generic_ex(c, false, false, n, n, n, 1.0, s.R, lc, s.Racc, lc, 0.0, s.tmp, lc, s.partials, s.partial_elems,
-                    false, nullptr, 0);
+    gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, s.tmp, lc, s.partials, s.partial_elems);
     launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, nullptr, 0);
   }
   // pass 3 (only when pass 1 or 2 needed the shift, bits 1<<8 | 2<<8, or completed dependent
@@ -543,8 +542,7 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded, true);
   launch_copy(c, m, n, s.Ybuf, s.ldy, V, ldv, false, condw, m3);
   if (R) {
-    gemm_generic_ex(c, false, false, n, n, n, 1.0, s.R, lc, s.Racc, lc, 0.0, s.tmp, lc, s.partials, s.partial_elems,
-                    false, condw, m3);
+    gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, s.tmp, lc, s.partials, s.partial_elems, condw, m3);
     launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, condw, m3);
     launch_copy(c, n, n, s.Racc, lc, R, ldr, false, nullptr, 0);
     // with completed columns Y = V R no longer holds for R2 R1: R = V^T Y (upper triangular in

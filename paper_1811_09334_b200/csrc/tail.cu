@@ -126,8 +126,7 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
       launch_copy(c, l, l, Rcur, ldl, s.Mt, ldl, true);      // [R^(i-1)]^T
       orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, s.Lt, ldl, false);
       if (i % 2 == 0) {
-        gemm_generic_ex(c, false, false, l, l, l, 1.0, s.QE, ldl, s.Qt, ldl, 0.0, s.tmp_ll, ldl, s.orth.partials,
-                        s.orth.partial_elems, false, nullptr, 0);
+        gemm_nn(c, l, l, l, s.QE, ldl, s.Qt, ldl, s.tmp_ll, ldl, s.orth.partials, s.orth.partial_elems);
         launch_copy(c, l, l, s.tmp_ll, ldl, s.QE, ldl, false);
       } else {
         gemm_nn(c, n, l, l, PO, ldn, s.Qt, ldl, Pspare, ldn, s.orth.partials, s.orth.partial_elems);
