@@ -532,19 +532,15 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   // pass 1: Y -> Ybuf (R1 in Racc), pass 2: Ybuf -> V (R2 in R)
   cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
   cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded, true);
-  if (R) {  // R = R2 R1
-    gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, s.tmp, lc, s.partials, s.partial_elems);
-    launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, nullptr, 0);
-  }
+  if (R) gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, R, ldr, s.partials, s.partial_elems);  // R = R2 R1
   // pass 3 (only when pass 1 or 2 needed the shift, bits 1<<8 | 2<<8, or completed dependent
   // columns, bits 1<<16 | 2<<16): V -> Ybuf -> V
   const unsigned m3 = (1u << 8) | (2u << 8) | (1u << 16) | (2u << 16);
   cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded, true);
   launch_copy(c, m, n, s.Ybuf, s.ldy, V, ldv, false, condw, m3);
   if (R) {
-    gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, s.tmp, lc, s.partials, s.partial_elems, condw, m3);
-    launch_copy(c, n, n, s.tmp, lc, s.Racc, lc, false, condw, m3);
-    launch_copy(c, n, n, s.Racc, lc, R, ldr, false, nullptr, 0);
+    gemm_nn(c, n, n, n, s.R, lc, R, ldr, s.tmp, lc, s.partials, s.partial_elems, condw, m3);  // R3 R2 R1
+    launch_copy(c, n, n, s.tmp, lc, R, ldr, false, condw, m3);
     // with completed columns Y = V R no longer holds for R2 R1: R = V^T Y (upper triangular in
     // exact arithmetic, zero rows for the completed directions)
     const unsigned mdep = (1u << 16) | (2u << 16) | (4u << 16);

@@ -116,27 +116,25 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
   if (d == 0) {
     PO = pivoted_lq(c, s, l, l, n, s.Q0, ldl, T, ldt, QB, ldqb, piv1);
   } else {
-    launch_copy(c, l, l, s.Q0, ldl, s.QE, ldl, false);
     PO = s.Qhat;
     double *Pspare = s.tmp_nl;
-    double *Rcur = s.Rhat;
+    double *qe = s.Q0, *qe_spare = s.QE;  // Q^(0) Q^(2) ..., ping-pong (no copies)
     for (int i = 2; i <= d; ++i) {
       // [Q^(i), R^(i)] = qr([R^(i-1)]^T): unpivoted, so CholeskyQR2 gives the same unique
-      // factors (R_ii > 0) as Householder to rounding (reading R3).
-      launch_copy(c, l, l, Rcur, ldl, s.Mt, ldl, true);      // [R^(i-1)]^T
-      orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, s.Lt, ldl, false);
+      // factors (R_ii > 0) as Householder to rounding (reading R3).  R^(i) overwrites R^(i-1)
+      // in Rhat (the input is the transposed copy in Mt).
+      launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, true);   // [R^(i-1)]^T
+      orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, s.Rhat, ldl, false);
       if (i % 2 == 0) {
-        gemm_nn(c, l, l, l, s.QE, ldl, s.Qt, ldl, s.tmp_ll, ldl, s.orth.partials, s.orth.partial_elems);
-        launch_copy(c, l, l, s.tmp_ll, ldl, s.QE, ldl, false);
+        gemm_nn(c, l, l, l, qe, ldl, s.Qt, ldl, qe_spare, ldl, s.orth.partials, s.orth.partial_elems);
+        std::swap(qe, qe_spare);
       } else {
         gemm_nn(c, n, l, l, PO, ldn, s.Qt, ldl, Pspare, ldn, s.orth.partials, s.orth.partial_elems);
         std::swap(PO, Pspare);
       }
-      launch_copy(c, l, l, s.Lt, ldl, s.Rhat, ldl, false);
-      Rcur = s.Rhat;
     }
-    launch_copy(c, l, l, Rcur, ldl, T, ldt, d % 2 == 1);   // T = [R^(d)]^T (odd d) or R^(d) (even d)
-    launch_copy(c, l, l, s.QE, ldl, QB, ldqb, false);
+    launch_copy(c, l, l, s.Rhat, ldl, T, ldt, d % 2 == 1);   // T = [R^(d)]^T (odd d) or R^(d) (even d)
+    launch_copy(c, l, l, qe, ldl, QB, ldqb, false);
     if (piv1) {
       iota_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, piv1);
       RQLP_LAUNCHED(c);
