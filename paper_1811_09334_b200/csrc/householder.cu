@@ -461,15 +461,23 @@ __global__ void extract_r_kernel(int steps, int cols, const double *M, int64_t l
 template <bool VSMEM, bool QSMEM>
 __global__ void form_q_kernel(int rows, int steps, const double *Vst, const double *tau, const double *beta,
                               double *Q, int64_t ldq) {
-  extern __shared__ double fsm[];
+  extern __shared__ __align__(16) double fsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double *vs = fsm;
   double *qs = fsm + (VSMEM ? (int64_t)rows * steps : 0) + (int64_t)warp * rows;
   __shared__ double taus[1056];
-  const int tmax = min(steps, (int)((blockIdx.x + 1) * nw * 1));  // unused guard
-  (void)tmax;
-  if (VSMEM)
-    for (int64_t e = threadIdx.x; e < (int64_t)rows * steps; e += blockDim.x) vs[e] = Vst[e];
+  if (VSMEM) {
+    // stage only the reflectors this CTA's columns use (j <= its largest t), 16-byte loads,
+    // unrolled so many are in flight (one CTA streams up to rows x steps doubles)
+    const int tlast = min(steps - 1, (int)((gridDim.x * nw) * ((steps - 1) / (gridDim.x * nw)) +
+                                           (blockIdx.x + 1) * nw - 1));
+    const int64_t cnt = (int64_t)rows * (tlast + 1), cnt2 = cnt >> 1;
+    const double2 *src = reinterpret_cast<const double2 *>(Vst);
+    double2 *dst = reinterpret_cast<double2 *>(vs);
+#pragma unroll 8
+    for (int64_t e = threadIdx.x; e < cnt2; e += blockDim.x) dst[e] = src[e];
+    if ((cnt & 1) && threadIdx.x == 0) vs[cnt - 1] = Vst[cnt - 1];
+  }
   for (int e = threadIdx.x; e < steps && e < 1056; e += blockDim.x) taus[e] = tau[e];
   __syncthreads();
   const double *V = VSMEM ? vs : Vst;
