@@ -44,6 +44,8 @@ struct rqlp_handle_s {
   std::map<std::string, int> seen;
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t side = nullptr;  // Ctx::branch() stream and its fork/join events
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
   bool trace_free = getenv("RQLP_ENGINE_TRACE") == nullptr;
 };
@@ -95,6 +97,14 @@ Ctx make_ctx(rqlp_handle_t h) {
   c.comm = h->comm;
   c.rank = h->rank;
   c.nranks = h->nranks;
+  if (!h->side) {
+    RQLP_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  }
+  c.side = h->side;
+  c.ev_fork = h->ev_fork;
+  c.ev_join = h->ev_join;
   if (getenv("RQLP_ENGINE_TRACE")) {
     if (!g_trace) cudaMalloc(&g_trace, 4 * 4096 * sizeof(unsigned long long));
     c.trace = g_trace;
@@ -656,6 +666,9 @@ int rqlp_destroy(rqlp_handle_t h) {
   }
   for (auto ev : h->eager_pool) cudaEventDestroy(ev);
   if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->own) cudaFree(h->own);

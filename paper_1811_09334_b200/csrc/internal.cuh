@@ -104,6 +104,24 @@ struct Ctx {
   int rank = 0, nranks = 1;
   int64_t collectives = 0;
   unsigned long long *trace = nullptr;  // debug: engine phase timestamps
+  // a second stream for independent branches (fork/join by events; inside a CUDA-graph capture
+  // the branch becomes a parallel path of the graph)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  Ctx branch() const {  // a context on the side stream, after the work enqueued so far
+    if (cudaEventRecord(ev_fork, stream) != cudaSuccess || cudaStreamWaitEvent(side, ev_fork, 0) != cudaSuccess)
+      throw CudaError("fork failed");
+    Ctx b = *this;
+    b.stream = side;
+    b.timing = false;
+    b.launches = 0;
+    return b;
+  }
+  void join(const Ctx &b) {  // the main stream waits for the branch's work
+    if (cudaEventRecord(ev_join, side) != cudaSuccess || cudaStreamWaitEvent(stream, ev_join, 0) != cudaSuccess)
+      throw CudaError("join failed");
+    launches += b.launches;
+  }
 };
 
 // ---- NCCL (comm.cu) ----

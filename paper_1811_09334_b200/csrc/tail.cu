@@ -107,10 +107,14 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
   copy_i64_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, s.hh.perm, s.perm0);
   RQLP_LAUNCHED(c);
   hh_extract_r(c, s.hh, l, n, B, ldb, s.Rt, ldn, true);   // R0^T, n x l
-  hh_form_q(c, s.hh, l, n, s.Q0, ldl);                      // Q0, l x l
+  // Q0 (l x l) is needed only at the assembly: formed on the side stream while the main stream
+  // orthonormalises R0^T (the join precedes the next use of the reflector store s.hh)
+  Ctx side = c.branch();
+  hh_form_q(side, s.hh, l, n, s.Q0, ldl);
   c.mark("tail_cpqr_B");
   // R0^T = Q^ R^ (CholeskyQR2; the tall part of cpqr(R0^T) / the i = 1 inner QR)
   orth(c, s.orth, n, l, s.Rt, ldn, s.Qhat, ldn, s.Rhat, ldl);
+  c.join(side);
   c.mark("tail_qr_R0T");
   double *PO;
   if (d == 0) {
