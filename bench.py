@@ -59,26 +59,78 @@ def passes(c) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every ~2 ms by NVML in a background
+    thread; the summary keeps the samples taken inside the timed region (the `with` block; the
+    nearest later sample if the region is shorter than the period).  nvidia-smi is the fallback
+    when NVML is unavailable."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []   # (t, sm_mhz, reasons)
+        self.mx = None
+        self.nv = None
+        self.thread = None
+        self.stop = False
         self.p = None
+        self.out = ""
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            bus = torch.cuda.get_device_properties(self.index).pci_bus_id
+            dom = torch.cuda.get_device_properties(self.index).pci_domain_id
+            dev = torch.cuda.get_device_properties(self.index).pci_device_id
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev:02x}.0")
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _loop(self, nv, h):
+        while not self.stop:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                rs = [nm for nm, attr in self.REASONS if bits & getattr(nv, attr, 0)]
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import threading
+            nv, h = self._nvml_handle()
+            self.nv = nv
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            while not self.samples:
+                time.sleep(0.001)
         except Exception:
-            self.p = None
+            self.nv = None
+            try:
+                self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.p = None
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
-        self.out = ""
+        self.t1 = time.perf_counter()
+        if self.thread is not None:
+            while not any(t >= self.t0 for t, _, _ in self.samples):
+                time.sleep(0.001)
+            self.stop = True
+            self.thread.join(timeout=1)
         if self.p is not None:
             time.sleep(0.25)
             self.p.terminate()
@@ -89,8 +141,15 @@ class ClockSampler:
         return False
 
     def summary(self) -> dict:
+        if self.nv is not None:
+            inside = [s for s in self.samples if self.t0 <= s[0] <= self.t1]
+            if not inside:
+                inside = [min((s for s in self.samples if s[0] >= self.t0), key=lambda s: s[0])]
+            reasons = sorted({r for _, _, rs in inside for r in rs})
+            return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": self.mx,
+                    "reasons": reasons, "samples": len(inside), "source": "nvml"}
         sms, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = [nm for nm, _ in self.REASONS]
         for line in (self.out or "").splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 6:
@@ -104,7 +163,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms), "source": "nvidia-smi"}
 
 
 def flush_l2(buf: torch.Tensor):
