@@ -353,3 +353,31 @@ def test_brqlp_q0_two_passes(rq, orc):
     _check_factorization(rq, orc, A, g, o, k + p)
     passes = [nm for nm in names if nm.startswith("pass_")]
     assert passes == ["pass_sketch", "pass_project"], passes
+
+
+def test_pivot_ties_duplicate_columns(rq, orc):
+    """Exact ties (duplicate columns, equal norms): CPQR breaks them toward the lowest original
+    column index (reading R5) in both implementations, for RQLP and the truncated QLP."""
+    rng = np.random.default_rng(77)
+    A = rng.standard_normal((300, 120)) @ np.diag(np.logspace(0, -3, 120))
+    A[:, 40] = A[:, 3]
+    A[:, 90] = A[:, 3]
+    A[:, 11] = -A[:, 7]          # equal norms, opposite signs
+    A = np.asfortranarray(A)
+    g = rq.factorize(_cm(A), 20, 6, q=1, d=0, seed=2)
+    o = orc.rqlp(A, 20, 6, q=1, d=0, seed=2)
+    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"])
+    gt, ot = rq.tqlp(_cm(A), 26), orc.tqlp(A, 26)
+    assert np.array_equal(gt["piv0"].cpu().numpy(), ot["piv0"])
+    assert np.array_equal(gt["piv1"].cpu().numpy(), ot["piv1"])
+
+
+@pytest.mark.parametrize("b,l_max,q", [(10, 95, 2), (33, 99, 0)])
+def test_autorank_ragged_and_power(rq, orc, b, l_max, q):
+    """Auto-rank with a block size that does not divide l_max and with power steps."""
+    sig = np.arange(1, 301.0) ** -1.2
+    A = _rand_svd(700, 300, sig, 4242)
+    g = rq.autorank(_cm(A), b=b, l_max=l_max, eps=5e-2, q=q, seed=8)
+    o = orc.autorank(A, b=b, l_max=l_max, eps=5e-2, q=q, seed=8)
+    assert g["l"] == o["l"]
+    _check_factorization(rq, orc, A, g, o, g["l"])
