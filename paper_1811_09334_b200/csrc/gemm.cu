@@ -212,10 +212,10 @@ void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
 // ---- tall-skinny passes ------------------------------------------------------------------
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
                  int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask);
+                 unsigned cond_mask, int tri);
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
                  int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
-                 const unsigned *cond, unsigned cond_mask);
+                 const unsigned *cond, unsigned cond_mask, int tri);
 size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms);
 
 size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
@@ -227,16 +227,17 @@ size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
 
 void gemm_nn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X, int64_t ldx,
              double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-             unsigned cond_mask) {
-  if (gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask)) return;
+             unsigned cond_mask, int tri) {
+  if (gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri)) return;
   gemm_generic_ex(c, false, false, m, cc, k, 1.0, A, lda, X, ldx, 0.0, Y, ldy, partials, partial_elems, false, cond,
                   cond_mask);
 }
 
 void gemm_tn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
              double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
-             unsigned cond_mask) {
-  if (gemm_tn_tma(c, m, cc, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask)) return;
+             unsigned cond_mask, int tri) {
+  if (gemm_tn_tma(c, m, cc, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask, tri))
+    return;
   // Z (k x cc) = A^T V : op(A) = A^T (k x m), op(B) = V (m x cc)
   gemm_generic_ex(c, true, false, k, cc, m, 1.0, A, lda, V, ldv, 0.0, Z, ldz, partials, partial_elems, trans_out,
                   cond, cond_mask);

@@ -77,8 +77,12 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(NCONS * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
-                    double *__restrict__ part, const unsigned *cond, unsigned cond_mask) {
+                    double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri) {
   if (cond && ((*cond) & cond_mask) == 0) return;
+  // tri == 1: only the upper triangle of the (symmetric) output is wanted -- tiles strictly below
+  // the diagonal do nothing (a Gram; consumers read the upper triangle).  tri == 2: the B operand
+  // is upper triangular -- k-tiles at or beyond n0 + BN contribute nothing (Y R^-1).
+  if (tri == 1 && (int)(blockIdx.y * BM) >= (int)(blockIdx.x * BN) + BN) return;
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int B_BYTES = BN * BK * 8;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -90,8 +94,9 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int kt0 = blockIdx.z * ktiles_per_split;
-  const int kt1 = min(ktiles_total, kt0 + ktiles_per_split);
-  const int nkt = kt1 - kt0;
+  const int klim = tri == 2 ? min(ktiles_total, (n0 + BN + BK - 1) / BK) : ktiles_total;
+  const int kt1 = min(klim, kt0 + ktiles_per_split);
+  const int nkt = max(0, kt1 - kt0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -282,7 +287,7 @@ int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap
 
 template <int BN, int MODE>
 void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask) {
+               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri) {
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
   smem_attr((const void *)gemm_tma_kernel<BN, MODE>, SMEM);
@@ -291,24 +296,24 @@ void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int 
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
   gemm_tma_kernel<BN, MODE><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
-                                                                       mask);
+                                                                       mask, tri);
   RQLP_LAUNCHED(c);
   if (S > 1) launch_reduce(c, M, N, S, part, 1.0, 0.0, C, ldc, trans, cond, mask);
 }
 
 template <int MODE>
 void dispatch(Ctx &c, int bn, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask) {
+              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri) {
   switch (bn) {
-    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
-    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask); break;
+    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
   }
 }
 
@@ -339,7 +344,7 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
 
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X, int64_t ldx,
                  double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask) {
+                 unsigned cond_mask, int tri) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
   int bn = choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms);
   CUtensorMap ma, mb;
@@ -348,13 +353,13 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   int64_t ktiles = ceil_div(k, BK);
   int64_t tiles = ceil_div(m, BM) * ceil_div(cc, bn);
   int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn);
-  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask);
+  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri);
   return true;
 }
 
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
                  double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask) {
+                 unsigned cond_mask, int tri) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
   int bn = choose_bn_mk(k, cc, ceil_div(m, BK), c.num_sms);
   CUtensorMap ma, mb;
@@ -362,8 +367,13 @@ bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (!make_map(&mb, V, m, cc, ldv, BK, bn)) return false;
   int64_t ktiles = ceil_div(m, BK);
   int64_t tiles = ceil_div(k, BM) * ceil_div(cc, bn);
+  if (tri == 1) {  // only tiles reaching the upper triangle do work
+    tiles = 0;
+    for (int64_t mt = 0; mt < ceil_div(k, BM); ++mt)
+      for (int64_t nt = 0; nt < ceil_div(cc, bn); ++nt) tiles += (mt * BM < nt * bn + bn) ? 1 : 0;
+  }
   int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn);
-  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask);
+  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri);
   return true;
 }
 

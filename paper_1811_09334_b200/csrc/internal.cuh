@@ -152,14 +152,16 @@ void launch_omega(Ctx &c, int64_t n, int64_t l, int64_t col0, uint64_t seed, dou
 void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
                   int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
                   const unsigned *cond = nullptr, unsigned cond_mask = 0);
-// Y = A X  (A m x k, X k x c): tall-skinny pass.  Scratch for split-K partials.
+// Y = A X  (A m x k, X k x c): tall-skinny pass.  Scratch for split-K partials.  tri = 2: X is
+// upper triangular (k-tiles past the diagonal are skipped; a hint -- the result is the same).
 void gemm_nn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
              int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems,
-             const unsigned *cond = nullptr, unsigned cond_mask = 0);
-// Z = A^T V (k x c) or Z^T (c x k) when trans_out.
+             const unsigned *cond = nullptr, unsigned cond_mask = 0, int tri = 0);
+// Z = A^T V (k x c) or Z^T (c x k) when trans_out.  tri = 1: a symmetric product (Gram) of which
+// only the upper triangle is needed -- the strictly lower part of Z is then left undefined.
 void gemm_tn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
              int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
-             const unsigned *cond = nullptr, unsigned cond_mask = 0);
+             const unsigned *cond = nullptr, unsigned cond_mask = 0, int tri = 0);
 size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms);
 
 // ---- small dense (dense.cu) ----

@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(1024) near_identity_kernel(int n, const double
   const int64_t total = (int64_t)n * n;
   for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
     const int i = (int)(e % n), j = (int)(e / n);
+    if (i > j) continue;  // the Gram's upper triangle (the lower one is not formed)
     const double v = G[i + (int64_t)j * ldg] - (i == j ? 1.0 : 0.0);
     emax = fmax(emax, fabs(v));
   }
@@ -483,7 +484,8 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   int64_t lc = round_up(n, 8);
   unsigned *condw = c.dflags + COND_WORD;
   const unsigned dep_bit = pass_bit << 16;
-  gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask);
+  // Gram (upper triangle only: every consumer below reads G(a, b) with a <= b)
+  gemm_tn(c, m, n, n, Yin, ldyi, Yin, ldyi, s.G, lc, false, s.partials, s.partial_elems, cond, mask, 1);
   if (sharded) allreduce_sum(c, s.G, lc * n);   // Gram summed over the row shards
   if (n <= CHOL_SMALL) {
     // one kernel: near-identity factor (second pass), else Cholesky + inverse, and on breakdown
@@ -510,7 +512,7 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
     chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, 0u, condw, pass_bit, s.partials,
              s.partial_elems, nullptr, 0u);
   }
-  gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, gcond, gmask);
+  gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, gcond, gmask, 2);  // R^-1 upper
   // rank-deficient columns -> random completion, orthonormalised by the following pass
   replace_dep_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
                            (unsigned)std::min<int64_t>(n, 64)),
