@@ -24,6 +24,7 @@ namespace rqlpk {
 namespace {
 
 constexpr double TOL3Z = 1.0536712127723509e-08;  // sqrt(2^-53), LAPACK dlaqp2 tol3z
+constexpr int RPL = 40;  // rows per lane kept in registers for global-memory columns (<= 1281 rows)
 
 struct Best {
   double v;
@@ -94,7 +95,7 @@ __device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
 // downdates their norms; warps post their best candidate in a parity-double-buffered slot and
 // meet at the step's single __syncthreads; every warp then reduces the 32 slots itself.
 template <bool GRID, bool SMEMC>
-__global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engine_kernel(EngineArgs a) {
   extern __shared__ __align__(16) double smem[];
   // even strides keep every cached column and the pivot column 16-byte aligned (double2 access
   // in absolute row coordinates); the padding row is zero and stays zero
@@ -328,15 +329,40 @@ __global__ void __launch_bounds__(GRID ? 512 : 1024) hh_engine_kernel(EngineArgs
                 *reinterpret_cast<double2 *>(cab + ar) = u;
               }
             }
+          } else if (len <= 1 + 32 * RPL) {
+            // columns in global memory, short enough to stay in registers for the step: one read
+            // and one write of the column (all loads in flight) instead of read, read, write
+            double reg[RPL];
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const int r = 1 + l8 + 32 * i;
+              reg[i] = r < len ? col[r] : 0.0;
+            }
+            double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < RPL; i += 2) {
+              const int r = 1 + l8 + 32 * i;
+              if (r < len) w0 = fma(cp[r] * scal, reg[i], w0);
+              if (i + 1 < RPL && r + 32 < len) w1 = fma(cp[r + 32] * scal, reg[i + 1], w1);
+            }
+            double w = gsum(w0 + w1);
+            w *= tau;
+            x -= w;  // the updated row-j entry (identical in the lanes)
+            if (l8 == 0) col[0] = x;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const int r = 1 + l8 + 32 * i;
+              if (r < len) col[r] = fma(-w, cp[r] * scal, reg[i]);
+            }
           } else {
-            // columns in global memory (L2): a simple strided loop the compiler unrolls, so many
-            // loads are in flight
+            // longer columns in global memory (L2): a simple strided loop the compiler unrolls, so
+            // many loads are in flight
             double w = l8 == 0 ? x : 0.0;
 #pragma unroll 8
             for (int r = 1 + l8; r < len; r += GS) w = fma(cp[r] * scal, col[r], w);
             w = gsum(w);
             w *= tau;
-            x -= w;  // the updated row-j entry (identical in the 8 lanes)
+            x -= w;  // the updated row-j entry (identical in the lanes)
             if (l8 == 0) col[0] = x;
 #pragma unroll 8
             for (int rr = 1 + l8; rr < len; rr += GS) col[rr] = fma(-w, cp[rr] * scal, col[rr]);
@@ -569,7 +595,7 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     // through cudaLaunchKernelEx (capturable into CUDA graphs)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(cached ? 512 : 256);  // global-memory columns: 256 threads, registers for the column
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
