@@ -17,9 +17,9 @@ import torch
 
 from . import _capi
 
-__all__ = ["Handle", "RQLPError", "rqlp", "erqlp", "brqlp", "factorize", "omega", "gemm_nn", "gemm_tn", "orth",
-           "cpqr", "qlp_tail", "residual", "rqlp_host", "cm_empty", "col_major", "lib", "VARIANT_RQLP",
-           "VARIANT_ERQLP", "VARIANT_BRQLP"]
+__all__ = ["Handle", "RQLPError", "rqlp", "erqlp", "brqlp", "factorize", "factorize_host", "autorank", "tqlp",
+           "omega", "gemm_nn", "gemm_tn", "orth", "cpqr", "qlp_tail", "residual", "rqlp_host", "cm_empty",
+           "col_major", "lib", "VARIANT_RQLP", "VARIANT_ERQLP", "VARIANT_BRQLP"]
 
 VARIANT_RQLP, VARIANT_ERQLP, VARIANT_BRQLP = 0, 1, 2
 FLAG_SHIFTED_CHOLQR = 1
