@@ -45,7 +45,7 @@ extern "C" {
 #define RQLP_VARIANT_BRQLP 2     /* Algorithm 3 */
 
 /* rqlp_sync() flag bits */
-#define RQLP_FLAG_SHIFTED_CHOLQR 1u  /* a shifted CholeskyQR3 pass was needed (ill-conditioned Y) */
+#define RQLP_FLAG_SHIFTED_CHOLQR 1u  /* a shifted CholeskyQR pass was needed (cond(Y) >~ 1e6) */
 #define RQLP_FLAG_RANK_DEFICIENT 2u  /* a basis column had to be completed (rank(Y) < l) */
 
 typedef struct rqlp_handle_s *rqlp_handle_t;
@@ -164,8 +164,10 @@ int rqlp_gemm_nn(rqlp_handle_t h, int64_t m, int64_t c, int64_t k, const double 
  * projection pass B = V^T A (Alg.1 l.4) and the power step A^T V. */
 int rqlp_gemm_tn(rqlp_handle_t h, int64_t m, int64_t c, int64_t k, const double *A, int64_t lda,
                  const double *V, int64_t ldv, double *Z, int64_t ldz, int trans_out);
-/* V = orth(Y) (m x c, c <= m): CholeskyQR2 with shifted CholeskyQR3 fallback (Alg.1 l.3,
- * PAPER.md:97); R (c x c upper, R_ii > 0, Y = V R) written when non-NULL. */
+/* V = orth(Y) (m x c, c <= m): CholeskyQR2; after a Cholesky breakdown (cond(Y) >~ 1e6, or
+ * rank(Y) < c), shifted CholeskyQR passes until V is orthonormal to working precision (Alg.1
+ * l.3).  R (c x c upper, Y = V R to O(u ||Y||); R_ii > 0 for full-rank Y) written
+ * when non-NULL. */
 int rqlp_orth(rqlp_handle_t h, int64_t m, int64_t c, const double *Y, int64_t ldy, double *V, int64_t ldv,
               double *R, int64_t ldr);
 /* Column-pivoted Householder QR of M (rows x cols), s = min(rows, cols) steps (Alg.1 l.5):

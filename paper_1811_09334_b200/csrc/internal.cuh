@@ -181,7 +181,11 @@ struct OrthScratch {
   int *dep = nullptr;           // dependent-column flags of the last Cholesky (rank deficiency)
 };
 void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms);
-// V = orth(Y) (CholeskyQR2 + conditional shifted pass).  Y is preserved; Y and V must not alias.  R (nullable) receives the c x c triangular factor (Y = V R).
+// orth's rare branch (orth_rescue.cu): if (*cond & mask), repeated (shifted) CholeskyQR passes on
+// V (m x n) until orthonormal, then R = V^T Y (nullable); one cooperative kernel.
+void launch_orth_rescue(Ctx &c, OrthScratch &s, int64_t m, int64_t n, double *V, int64_t ldv, const double *Y,
+                        int64_t ldy, double *R, int64_t ldr, const unsigned *cond, unsigned mask);
+// V = orth(Y) (CholeskyQR2; after a breakdown, shifted passes until orthonormal).  Y is preserved; Y and V must not alias.  R (nullable) receives the c x c triangular factor (Y = V R).
 // sharded: Y is a row block of a row-sharded matrix -> the Gram is summed over ranks.
 // span_only: an intermediate subspace-iteration basis (one CholeskyQR pass; V spans range(Y) but
 // is only approximately orthonormal).

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   __shared__ double wkk[2][64];  // W_KK[i][t] at wkk[.][i * 8 + t] (unit lower), double-buffered
   __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL], sq[CHOL_SMALL];
   __shared__ double red[16];
-  __shared__ int s_fail, s_dep;
+  __shared__ int s_fail, s_dep, s_tiny;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int npad = (n + 7) & ~7, nt = npad >> 3;
   // M(b, a) = G[a + b ldg] (+ shift on the diagonal) for a <= b: the lower part (read coalesced
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
       return;
     }
   }
-  if (tid == 0) { s_fail = 0; s_dep = 0; }
+  if (tid == 0) { s_fail = 0; s_dep = 0; s_tiny = 0; }
   __syncthreads();
   int *dep_att = dep;
   for (int attempt = 0;; ++attempt) {
@@ -180,9 +180,12 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         for (int p = 0; p < 8; ++p)
           if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
         const int kg = k0 + i;  // lane i records pivot i
-        double pv = piv[0];
+        double pv = piv[0], dr = d[0];
   #pragma unroll
-        for (int p = 1; p < 8; ++p) if (i == p) pv = piv[p];
+        for (int p = 1; p < 8; ++p) if (i == p) { pv = piv[p]; dr = d[p]; }
+        // a numerically dependent column (pivot <= 1e-15 of its diagonal before any shift):
+        // reported as RQLP_FLAG_RANK_DEFICIENT whether or not the column is completed here
+        if (attempt == 0 && kg < n && !(dr > CHOL_DEP * g0s[kg]) && !isnan(dr)) s_tiny = 1;
         dpiv[kg] = pv;
         dinv[kg] = fast_rcp(pv);
         const unsigned kind = (kinds >> (2 * i)) & 3u;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
     }
   }
   if (tid == 0 && s_fail) atomicOr(fail_word, fail_bit);
+  if (tid == 0 && s_tiny) atomicOr(flag_word, (unsigned)RQLP_FLAG_RANK_DEFICIENT);
   if (tid == 0 && s_dep && dep) {
     atomicOr(fail_word, dep_bit);
     atomicOr(flag_word, (unsigned)RQLP_FLAG_RANK_DEFICIENT);
@@ -478,7 +482,7 @@ void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms) {
 // breakdown in the COND word.  Kernels run only if (*cond & mask) when cond given.
 static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Yin, int64_t ldyi, double *Qout,
                         int64_t ldqo, double *Rout, unsigned pass_bit, const unsigned *cond, unsigned mask,
-                        bool sharded, bool second = false) {
+                        bool sharded, bool second = false, bool use_dep = true) {
   const unsigned *gcond = cond;   // the pass's own condition (the GEMMs)
   const unsigned gmask = mask;
   int64_t lc = round_up(n, 8);
@@ -490,8 +494,8 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   if (n <= CHOL_SMALL) {
     // one kernel: near-identity factor (second pass), else Cholesky + inverse, and on breakdown
     // the shifted retry in place (marks pass_bit << 8 for the third pass)
-    launch_chol_inv(c, (int)n, s.G, lc, s.G, lc, Rout, lc, s.Rinv, lc, condw, 0u, cond, mask, s.dep, dep_bit,
-                    second ? 1 : 0, (double)m, pass_bit << 8);
+    launch_chol_inv(c, (int)n, s.G, lc, s.G, lc, Rout, lc, s.Rinv, lc, condw, 0u, cond, mask,
+                    use_dep ? s.dep : nullptr, dep_bit, second ? 1 : 0, (double)m, pass_bit << 8);
   } else {
     if (second) {
       // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
@@ -503,7 +507,7 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
     }
     launch_copy(c, n, n, s.G, lc, s.G2, lc, false, cond, mask);  // blocked path destroys G
     chol_inv(c, n, s.G, lc, s.G2, lc, Rout, lc, s.Rinv, lc, s.tmp, condw, pass_bit, cond, mask, s.partials,
-             s.partial_elems, s.dep, dep_bit);
+             s.partial_elems, use_dep ? s.dep : nullptr, dep_bit);
     // breakdown (ill-conditioned) -> shifted Gram, second attempt (only if pass_bit was set)
     add_shift_kernel<<<1, 1024, 0, c.stream>>>((int)n, s.G2, lc, (double)m, c.dflags + FLAG_WORD, condw, pass_bit,
                                                pass_bit << 8);
@@ -513,6 +517,7 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
              s.partial_elems, nullptr, 0u);
   }
   gemm_nn(c, m, n, n, Yin, ldyi, s.Rinv, lc, Qout, ldqo, s.partials, s.partial_elems, gcond, gmask, 2);  // R^-1 upper
+  if (!use_dep) return;
   // rank-deficient columns -> random completion, orthonormalised by the following pass
   replace_dep_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
                            (unsigned)std::min<int64_t>(n, 64)),
@@ -528,10 +533,29 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
   if (span_only && !R) {
     // intermediate subspace-iteration basis: only range(V) = range(Y) matters (V = Y R^-1 for any
     // invertible R keeps the span to the same O(u cond(Y)) rounding), so one CholeskyQR pass.
+    if (!sharded) {
+      // a breakdown (shifted pass) leaves V far from orthonormal, with the small directions of Y
+      // compressed by ~s^-1/2: the next product A^T V would push them below the rounding level,
+      // so the rescue passes restore an orthonormal V first (Householder-quality basis)
+      cholqr_pass(c, s, m, n, Y, ldy, V, ldv, s.Racc, 1u, nullptr, 0, false, false, false);
+      launch_orth_rescue(c, s, m, n, V, ldv, Y, ldy, nullptr, 0, condw, 1u << 8);
+      return;
+    }
     cholqr_pass(c, s, m, n, Y, ldy, V, ldv, s.Racc, 1u, nullptr, 0, sharded);
     return;
   }
   // pass 1: Y -> Ybuf (R1 in Racc), pass 2: Ybuf -> V (R2 in R)
+  if (!sharded) {
+    // CholeskyQR2 without column completion (a tiny pivot is a breakdown: the shifted retry keeps
+    // every direction of Y); after any breakdown (bits 1<<8 | 2<<8) the rescue kernel continues
+    // with shifted passes until V is orthonormal and recomputes R = V^T Y
+    cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, false, false, false);
+    cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, false, true, false);
+    if (R) gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, R, ldr, s.partials, s.partial_elems);  // R = R2 R1
+    launch_orth_rescue(c, s, m, n, V, ldv, Y, ldy, R, ldr, condw, (1u << 8) | (2u << 8));
+    return;
+  }
+  // row-sharded: the Gram is an allreduce, so the rare branch stays a conditional third pass
   cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
   cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded, true);
   if (R) gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, R, ldr, s.partials, s.partial_elems);  // R = R2 R1

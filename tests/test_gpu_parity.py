@@ -85,6 +85,43 @@ def test_orth_matches_householder(rq, orc, m, c, cond):
     assert np.abs(R - Ro).max() <= max(tol, 1e-13) * np.abs(Ro).max()
 
 
+_RESCUE_SPECTRA = {
+    "graded1e-20": lambda c: np.logspace(0, -20, c),
+    "graded1e-39": lambda c: np.logspace(0, -39, c),
+    "rank_half": lambda c: np.r_[np.ones(c - c // 2), np.zeros(c // 2)],
+    "gap1e-9": lambda c: np.r_[np.ones(c - c // 3), 1e-9 * np.ones(c // 3)],
+    "one_big": lambda c: np.r_[np.ones(1), 1e-12 * np.ones(c - 1)],
+    "zero": lambda c: np.zeros(c),
+}
+
+
+@pytest.mark.parametrize("spec", sorted(_RESCUE_SPECTRA))
+@pytest.mark.parametrize("m,c", [(400, 16), (5000, 110), (3000, 200)])
+def test_orth_rescue(rq, orc, spec, m, c):
+    """cond(Y) far beyond CholeskyQR2's reach (or rank(Y) < c): CholeskyQR2 breaks down and the
+    rescue kernel's shifted passes must still return V with orthonormal columns and Y = V R to
+    O(u ||Y||), R upper triangular -- what Householder QR guarantees for any Y (the oracle's hqr:
+    the same bounds hold for it, checked alongside).  c = 200 runs the blocked Cholesky path."""
+    Y = _rand_svd(m, c, _RESCUE_SPECTRA[spec](c), m + 3 * c)
+    h = rq.Handle()
+    V, R = rq.orth(_cm(Y), return_r=True, handle=h)
+    flags = h.sync()
+    V, R = _np(V), _np(R)
+    nY = max(np.linalg.norm(Y, 2), 1e-300)
+    Qo, Ro = orc.hqr(Y)
+    for Qx, Rx in ((V, R), (Qo, Ro)):
+        assert np.abs(Qx.T @ Qx - np.eye(c)).max() <= 1e-14 * np.sqrt(c) * 10
+        assert np.abs(Qx @ Rx - Y).max() <= 1e-14 * max(nY, 1e-300) * 10 or spec == "zero"
+    assert not np.tril(R, -1).any()
+    if spec == "zero":
+        assert not R.any()
+    assert flags & 1  # the shifted passes ran
+    # the factor R agrees with Householder's on the leading, well-separated directions
+    if spec in ("gap1e-9", "rank_half"):
+        k = c - c // 2 if spec == "rank_half" else c - c // 3
+        np.testing.assert_allclose(np.abs(np.diag(R)[:k]), np.abs(np.diag(Ro)[:k]), rtol=1e-8)
+
+
 @pytest.mark.parametrize("rows,cols", [(25, 800), (110, 4096), (64, 5000), (40, 40), (30, 17)])
 def test_cpqr_parity(rq, orc, rows, cols):
     rng = np.random.default_rng(rows * cols)
@@ -381,3 +418,51 @@ def test_autorank_ragged_and_power(rq, orc, b, l_max, q):
     o = orc.autorank(A, b=b, l_max=l_max, eps=5e-2, q=q, seed=8)
     assert g["l"] == o["l"]
     _check_factorization(rq, orc, A, g, o, g["l"])
+
+
+# ------------------------------------------------------------------ graph replay of the rare branches
+def _zero(m, n, seed):
+    return np.zeros((m, n), order="F")
+
+
+def _deficient(m, n, seed):
+    return _rand_svd(m, n, np.array([3.0, 2.0, 1.0, 0.5, 0.25, 0.125]), seed)
+
+
+def _illcond(m, n, seed):
+    # rank 16 = l, cond(Y) ~ 1e13 > u^-1/2: the unshifted Cholesky breaks down, the shifted
+    # third pass runs
+    return _rand_svd(m, n, np.logspace(0, -13, 16), seed)
+
+
+def _wellcond(m, n, seed):
+    return _rand_svd(m, n, np.exp(-np.arange(1, min(m, n) + 1.0) / 20), seed)
+
+
+@pytest.mark.parametrize("make,flag,d", [(_zero, 2, 0), (_deficient, 2, 2), (_illcond, 1, 0), (_wellcond, 0, 2)])
+def test_graph_replay_branches(rq, orc, make, flag, d):
+    """Each call with the same arguments runs eagerly first, then as a captured CUDA graph whose
+    rare orth branches (random completion, third CholeskyQR pass) are conditional nodes opened
+    on the device.  Eager and replayed results must be bitwise identical and flag the branch."""
+    A = make(400, 300, 5)
+    h = rq.Handle()
+    At = _cm(A)
+    res, ptrs, flags = [], set(), []
+    for _ in range(4):
+        g = rq.factorize(At, 12, 4, q=1, d=d, seed=7, handle=h)
+        flags.append(h.sync())
+        ptrs.add(tuple(g[k].data_ptr() for k in ("Q", "T", "P")))
+        res.append({k: _np(g[k]) for k in ("Q", "T", "P")})
+        del g
+    assert len(ptrs) == 1  # same buffers -> calls 2..4 are capture + replays of one graph
+    for r in res[1:]:
+        for k in ("Q", "T", "P"):
+            np.testing.assert_array_equal(r[k], res[0][k])
+    assert all((f & flag) == flag and (flag or not f & 3) for f in flags), flags
+    Q, T, P = res[0]["Q"], res[0]["T"], res[0]["P"]
+    assert np.abs(Q.T @ Q - np.eye(16)).max() <= 1e-12
+    # the residual of the oracle on the same input bounds ours (rank(A) <= l: both ~ exact, up to
+    # the directions the power step pushes below the rounding level of Y)
+    o = orc.rqlp(A, 12, 4, q=1, d=d, seed=7)
+    ro = orc.residual(A, o["Q"], o["T"], o["P"])
+    assert orc.residual(A, Q, T, P) <= 10 * ro + 1e-13 * max(np.linalg.norm(A), 1.0)
