@@ -77,7 +77,8 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(NCONS * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
-                    double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri) {
+                    double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri, int bal_units,
+                    int ntn, int maxc) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   // tri == 1: only the upper triangle of the (symmetric) output is wanted -- tiles strictly below
   // the diagonal do nothing (a Gram; consumers read the upper triangle).  tri == 2: the B operand
@@ -92,11 +93,37 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
   uint64_t *empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-  const int kt0 = blockIdx.z * ktiles_per_split;
-  const int klim = tri == 2 ? min(ktiles_total, (n0 + BN + BK - 1) / BK) : ktiles_total;
-  const int kt1 = min(klim, kt0 + ktiles_per_split);
-  const int nkt = max(0, kt1 - kt0);
+  // balanced split (bal_units > 0, tri == 0): the (tile, k-tile) units in tile-major order are
+  // dealt out in equal contiguous runs of bal_units, one run per CTA (grid = #SMs); a run spans
+  // at most a few tiles and each tile segment's partial goes to slot (tile, CTA - first CTA of
+  // the tile), summed in slot order by bal_reduce_kernel.  Otherwise grid = (N tiles, M tiles,
+  // split-K slices).
+  const bool bal = bal_units > 0;
+  const int n0 = bal ? 0 : blockIdx.x * BN, m0 = bal ? 0 : blockIdx.y * BM;
+  const int kt0 = bal ? 0 : blockIdx.z * ktiles_per_split;
+  const int u0 = bal ? blockIdx.x * bal_units : 0;
+  int nkt;
+  if (bal) {
+    const int total = ktiles_total * ntn * ((M + BM - 1) / BM);
+    nkt = max(0, min(total, u0 + bal_units) - u0);
+  } else {
+    const int klim = tri == 2 ? min(ktiles_total, (n0 + BN + BK - 1) / BK) : ktiles_total;
+    const int kt1 = min(klim, kt0 + ktiles_per_split);
+    nkt = max(0, kt1 - kt0);
+  }
+  // (tile origin, k offset) of pipeline iteration it
+  auto coords = [&](int it, int &tm0, int &tn0, int &kk) {
+    if (bal) {
+      const int u = u0 + it, t = u / ktiles_total, kt = u - t * ktiles_total;
+      tm0 = (t / ntn) * BM;
+      tn0 = (t % ntn) * BN;
+      kk = kt * BK;
+    } else {
+      tm0 = m0;
+      tn0 = n0;
+      kk = (kt0 + it) * BK;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -112,11 +139,12 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
     const int s = it % STAGES;
     unsigned char *sa = smem + s * STAGE_BYTES;
     unsigned char *sb = sa + A_BYTES;
-    const int kk = (kt0 + it) * BK;
+    int tm0, tn0, kk;
+    coords(it, tm0, tn0, kk);
     mbar_expect_tx(&full[s], (MODE == 0 ? BK * LDA_NN * 8 : A_TILE_BYTES_TN) + B_BYTES);
-    if (MODE == 0) tma_load_2d(sa, &mapA, m0, kk, &full[s]);   // A box {BM+2, BK} at (m0, k)
-    else tma_load_2d(sa, &mapA, kk, m0, &full[s]);             // A box {BK, BM} at (k = row offset, col)
-    tma_load_2d(sb, &mapB, kk, n0, &full[s]);                  // B box {BK, BN} at (k, n0)
+    if (MODE == 0) tma_load_2d(sa, &mapA, tm0, kk, &full[s]);   // A box {BM+2, BK} at (m0, k)
+    else tma_load_2d(sa, &mapA, kk, tm0, &full[s]);             // A box {BK, BM} at (k = row offset, col)
+    tma_load_2d(sb, &mapB, kk, tn0, &full[s]);                  // B box {BK, BN} at (k, n0)
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapA) : "memory");
@@ -171,7 +199,25 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (bal && (it + 1 == nkt || (u0 + it + 1) % ktiles_total == 0)) {
+      // end of a tile segment: its partial tile (all BM x BN entries) to the tile's slot
+      const int t = (u0 + it) / ktiles_total;
+      const int slot = blockIdx.x - (int)(((long long)t * ktiles_total) / bal_units);
+      double *dst = part + ((size_t)t * maxc + slot) * (BM * BN);
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const int il = wm * 32 + mb * 8 + r;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          const int jl = wn * (BN / 2) + nb * 8 + 2 * cq;
+          dst[il + jl * BM] = acc[mb][nb][0];
+          dst[il + (jl + 1) * BM] = acc[mb][nb][1];
+          acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+        }
+      }
+    }
   }
+  if (bal) return;
 
   // ---------------- epilogue: fragment (mb, nb) holds out[row][col], out[row][col+1]
 #pragma unroll
@@ -198,6 +244,33 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
         if (j + 1 < N) C[i + (size_t)(j + 1) * ldc] = acc[mb][nb][1];
       }
     }
+  }
+}
+
+// Sum of a balanced split's slots: element (i, j) of tile t = (i / BM) ntn + j / bn is the sum,
+// in slot order, of the partial tiles of the CTAs first(t) .. last(t) whose runs touch t.
+__global__ void bal_reduce_kernel(int M, int N, int bn, int ntn, int ktiles, int units, int maxc,
+                                  const double *__restrict__ part, double *__restrict__ C, int64_t ldc, int trans,
+                                  const unsigned *cond, unsigned cond_mask) {
+  if (cond && ((*cond) & cond_mask) == 0) return;
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    if (trans) {  // consecutive threads along j: coalesced stores into C^T
+      i = (int)(e / N);
+      j = (int)(e % N);
+    } else {
+      i = (int)(e % M);
+      j = (int)(e / M);
+    }
+    const int mt = i / BM, nt = j / bn, t = mt * ntn + nt;
+    const int first = (int)(((long long)t * ktiles) / units);
+    const int last = (int)(((long long)(t + 1) * ktiles - 1) / units);
+    const double *p = part + (size_t)t * maxc * (BM * bn) + (i - mt * BM) + (size_t)(j - nt * bn) * BM;
+    double sum = 0.0;
+    for (int q = 0; q <= last - first; ++q) sum += p[(size_t)q * (BM * bn)];
+    if (trans) C[j + (int64_t)i * ldc] = sum;
+    else C[i + (int64_t)j * ldc] = sum;
   }
 }
 
@@ -266,7 +339,8 @@ int choose_bn_mk(int64_t M, int64_t c, int64_t ktiles, int num_sms) {
 // Split-K: minimise the modelled time  waves(T) * ceil(ktiles / S) * t_ktile
 //                                      + (S > 1) * (2 S M N 8 bytes / HBM + reduce launch)
 // with T = tiles * S CTAs (1 CTA per SM), t_ktile = 128 BN 24 2 flop / (DMMA peak per SM).
-int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems, int bn) {
+int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems, int bn,
+                  double *t_out = nullptr) {
   const double t_ktile = 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);   // s
   const double hbm = 6.0e12;                                           // B/s
   int best = 1;
@@ -282,39 +356,87 @@ int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap
       best = s;
     }
   }
+  // the chosen split's time with the pipeline ramp (3 k-tiles per wave), comparable to the
+  // balanced model below
+  if (t_out) *t_out = best_t + (double)ceil_div(tiles * best, num_sms) * 3.0 * t_ktile;
   return best;
+}
+
+// Balanced split (see gemm_tma_kernel): units = ceil(tiles ktiles / #SMs) k-tiles per CTA.  Returns
+// the run length when its modelled time beats the split-K time t_split (and the slots fit), else 0.
+struct BalPlan {
+  int units = 0, maxc = 0;
+};
+BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int bn, double t_split) {
+  BalPlan p;
+  const int64_t total = tiles * ktiles;
+  if (tiles >= num_sms || total < 4 * (int64_t)num_sms || total >= (1ll << 31)) return p;
+  const int64_t U = ceil_div(total, num_sms);
+  int64_t maxc = 0;
+  for (int64_t t = 0; t < tiles; ++t) maxc = std::max<int64_t>(maxc, ((t + 1) * ktiles - 1) / U - (t * ktiles) / U + 1);
+  if ((size_t)(tiles * maxc * BM * bn) > partial_cap_elems) return p;
+  const double t_ktile = 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);
+  const double hbm = 6.0e12;
+  const double t = (double)(U + 3) * t_ktile + 2.0 * (double)(tiles + num_sms) * BM * bn * 8.0 / hbm + 4e-6;
+  if (t < 0.9 * t_split) {  // measured: a 5% gain at C2 (c = 110), a loss at c <= 40
+    p.units = (int)U;
+    p.maxc = (int)maxc;
+  }
+  return p;
 }
 
 template <int BN, int MODE>
 void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri) {
+               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp) {
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
   smem_attr((const void *)gemm_tma_kernel<BN, MODE>, SMEM);
+  if (bp.units > 0) {
+    const int ntn = (int)ceil_div(N, BN);
+    const int64_t total = (int64_t)ktiles * ntn * ceil_div(M, BM);
+    const unsigned ctas = (unsigned)ceil_div(total, bp.units);
+    gemm_tma_kernel<BN, MODE><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
+                                                                     part, cond, mask, 0, bp.units, ntn, bp.maxc);
+    RQLP_LAUNCHED(c);
+    const int grid = (int)std::min<int64_t>(ceil_div((int64_t)M * N, 256), (int64_t)c.num_sms * 16);
+    bal_reduce_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(M, N, BN, ntn, ktiles, bp.units, bp.maxc, part, C, ldc,
+                                                                trans ? 1 : 0, cond, mask);
+    RQLP_LAUNCHED(c);
+    return;
+  }
   int kps = (int)ceil_div(ktiles, S);
   S = (int)ceil_div(ktiles, kps);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
   gemm_tma_kernel<BN, MODE><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
-                                                                       mask, tri);
+                                                                       mask, tri, 0, 1, 1);
   RQLP_LAUNCHED(c);
   if (S > 1) launch_reduce(c, M, N, S, part, 1.0, 0.0, C, ldc, trans, cond, mask);
 }
 
 template <int MODE>
 void dispatch(Ctx &c, int bn, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri) {
+              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp) {
   switch (bn) {
-    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
-    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri); break;
+    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
   }
+}
+
+bool balanced_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RQLP_GEMM_BALANCED");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 bool tma_disabled() {
@@ -336,8 +458,11 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
     int64_t ktiles = ceil_div(K, BK);
     int bn = choose_bn_mk(M, cc, ktiles, num_sms);
     int64_t tiles = ceil_div(M, BM) * ceil_div(cc, bn);
-    int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cc, bn);
+    double ts = 0.0;
+    int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cc, bn, &ts);
     if (S > 1) best = std::max(best, (size_t)S * M * cc);
+    BalPlan bp = choose_balanced(tiles, ktiles, num_sms, (size_t)1 << 62, bn, ts);
+    if (bp.units > 0) best = std::max(best, (size_t)tiles * bp.maxc * BM * bn);
   }
   return best;
 }
@@ -352,8 +477,12 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (!make_map(&mb, X, k, cc, ldx, BK, bn)) return false;
   int64_t ktiles = ceil_div(k, BK);
   int64_t tiles = ceil_div(m, BM) * ceil_div(cc, bn);
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn);
-  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri);
+  double ts = 0.0;
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn, &ts);
+  BalPlan bp;
+  if (tri == 0 && partials && !balanced_disabled())
+    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
+  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri, bp);
   return true;
 }
 
@@ -372,8 +501,12 @@ bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
     for (int64_t mt = 0; mt < ceil_div(k, BM); ++mt)
       for (int64_t nt = 0; nt < ceil_div(cc, bn); ++nt) tiles += (mt * BM < nt * bn + bn) ? 1 : 0;
   }
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn);
-  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri);
+  double ts = 0.0;
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn, &ts);
+  BalPlan bp;
+  if (tri == 0 && partials && !balanced_disabled())
+    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
+  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri, bp);
   return true;
 }
 

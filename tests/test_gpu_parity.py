@@ -45,8 +45,10 @@ def test_omega_bit_exact(rq, orc, n, l, seed):
     assert np.array_equal(Om.view(np.uint64), ref.view(np.uint64))
 
 
+# (2000, 3000, 40), (4100, 4100, 110), (2500, 2600, 200): fewer output tiles than SMs and many
+# k-tiles -> the balanced split (equal runs of (tile, k-tile) units per CTA, ragged at both ends)
 @pytest.mark.parametrize("m,k,c", [(1000, 800, 25), (1031, 1030, 110), (4133, 1029, 138), (517, 93, 17), (64, 64, 64),
-                                   (3, 5, 2)])
+                                   (3, 5, 2), (2000, 3000, 40), (4100, 4100, 110), (2500, 2600, 200)])
 def test_gemm_nn_parity(rq, orc, m, k, c):
     rng = np.random.default_rng(m + k + c)
     A, X = rng.standard_normal((m, k)), rng.standard_normal((k, c))
@@ -57,7 +59,8 @@ def test_gemm_nn_parity(rq, orc, m, k, c):
 
 
 @pytest.mark.parametrize("m,k,c,trans", [(1000, 800, 25, True), (1031, 1030, 110, False), (4133, 1029, 138, True),
-                                         (517, 93, 17, False), (5, 3, 2, True)])
+                                         (517, 93, 17, False), (5, 3, 2, True), (3000, 2000, 40, True),
+                                         (4100, 4100, 110, False), (4100, 4100, 110, True), (2600, 2500, 200, False)])
 def test_gemm_tn_parity(rq, orc, m, k, c, trans):
     rng = np.random.default_rng(m * 3 + k + c)
     A, V = rng.standard_normal((m, k)), rng.standard_normal((m, c))
