@@ -82,6 +82,24 @@ struct EngineArgs {
   int64_t *perm;
 };
 
+// Exchange words: gpu-scope relaxed accesses (every word carries its step tag, so no ordering
+// between words is needed; gpu scope instead of the system scope of volatile), 16-byte vectors
+// for the (lo, hi) halves of a candidate row and the (hi, lo) halves of a record's value.
+__device__ __forceinline__ void st_x2(unsigned long long *p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};\n" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void st_x1(unsigned long long *p, unsigned long long a) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"(a) : "memory");
+}
+__device__ __forceinline__ void ld_x2(const unsigned long long *p, unsigned long long &a, unsigned long long &b) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_x1(const unsigned long long *p) {
+  unsigned long long a;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(a) : "l"(p) : "memory");
+  return a;
+}
+
 __device__ __forceinline__ unsigned long long pack(unsigned hi, unsigned tag) {
   return ((unsigned long long)hi << 32) | tag;
 }
@@ -132,19 +150,17 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
     else if (jn < a.cols && jn % G == b) src = jn;
     if (src >= 0) {
       const double *sp = colptr((src - b) / G);
-      volatile unsigned long long *dst = a.cand + ((int64_t)par * G + b) * rows * 2;
+      unsigned long long *dst = a.cand + ((int64_t)par * G + b) * rows * 2;
       for (int r = jn + lane; r < rows; r += 32) {
         const unsigned long long bits = (unsigned long long)__double_as_longlong(sp[r]);
-        dst[2 * (r - jn)] = pack((unsigned)bits, tag);
-        dst[2 * (r - jn) + 1] = pack((unsigned)(bits >> 32), tag);
+        st_x2(dst + 2 * (r - jn), pack((unsigned)bits, tag), pack((unsigned)(bits >> 32), tag));
       }
     }
     if (lane == 0 && (a.pivot || src >= 0)) {
       const unsigned long long bits = (unsigned long long)__double_as_longlong(a.pivot ? c.v : 0.0);
-      volatile unsigned long long *rc = a.rec + ((int64_t)par * G + b) * 4;
-      rc[0] = pack((unsigned)(bits >> 32), tag);
-      rc[1] = pack((unsigned)bits, tag);
-      rc[2] = pack((unsigned)(a.pivot ? c.i : src), tag);
+      unsigned long long *rc = a.rec + ((int64_t)par * G + b) * 4;
+      st_x2(rc, pack((unsigned)(bits >> 32), tag), pack((unsigned)bits, tag));
+      st_x1(rc + 2, pack((unsigned)(a.pivot ? c.i : src), tag));
     }
   };
 
@@ -199,8 +215,9 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
 #pragma unroll
             for (int t = 0; t < MAXR; ++t)
               if (pending & (1u << t)) {
-                volatile unsigned long long *rc = a.rec + ((int64_t)par * G + lane + 32 * t) * 4;
-                w0[t] = rc[0]; w1[t] = rc[1]; w2[t] = rc[2];
+                const unsigned long long *rc = a.rec + ((int64_t)par * G + lane + 32 * t) * 4;
+                ld_x2(rc, w0[t], w1[t]);
+                w2[t] = ld_x1(rc + 2);
               }
 #pragma unroll
             for (int t = 0; t < MAXR; ++t)
@@ -222,12 +239,11 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       }
       __syncthreads();
       p = s_p;
-      volatile const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * rows * 2;
+      const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * rows * 2;
       for (int r = threadIdx.x; r < len; r += blockDim.x) {
         unsigned long long lo, hi;
         do {
-          lo = src[2 * r];
-          hi = src[2 * r + 1];
+          ld_x2(src + 2 * r, lo, hi);
         } while ((unsigned)lo != tag || (unsigned)hi != tag);
         vraw[j + r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
       }
@@ -253,11 +269,6 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       const double rinv = fast_rcp(beta * amb);     // one reciprocal for both
       tau = -amb * amb * rinv;
       scal = beta * rinv;
-    }
-    if (b == 0 && warp == 0) {
-      double *vs = a.Vst + (int64_t)j * rows;
-      for (int r = lane; r < rows; r += 32) vs[r] = (r < j) ? 0.0 : (r == j ? 1.0 : cp[r - j] * scal);
-      if (lane == 0) { a.tau[j] = tau; a.beta[j] = beta; a.perm[j] = p; }
     }
     const int ob = p % G;
     if (b == ob && threadIdx.x == 0) {
@@ -428,6 +439,14 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       }
     } else if (GRID && warp == 0 && j + 1 < a.steps) {
       publish(j + 1, cta_best(par ^ 1));
+    }
+    // the reflector store, off the exchange's critical path: CTA j mod G, its last warp, after
+    // the publish (cp stays valid until the next step's fetch barrier).  Measured: written by
+    // CTA 0 before its update it delayed every step's slowest CTA by ~1000 cycles.
+    if (b == j % G && warp == wpb - 1) {
+      double *vs = a.Vst + (int64_t)j * rows;
+      for (int r = lane; r < rows; r += 32) vs[r] = (r < j) ? 0.0 : (r == j ? 1.0 : cp[r - j] * scal);
+      if (lane == 0) { a.tau[j] = tau; a.beta[j] = beta; a.perm[j] = p; }
     }
   }
   __syncthreads();
