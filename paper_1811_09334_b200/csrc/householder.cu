@@ -33,25 +33,21 @@ struct Best {
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
 
 // Warp argmax (max value, lowest index on ties).  Values are >= 0 (squared norms) or -1 (no
-// candidate); non-negative doubles order like their bit patterns, so one redux.sync on the high
-// 32 bits (biased so -1 sorts lowest) narrows the candidates, usually to a single lane.
+// candidate); non-negative doubles order like their bit patterns, so integer redux.sync on the
+// high then the low 32 bits (biased so -1 sorts lowest) finds the maximum, and one more on the
+// index picks the lowest among equal values -- no shuffle tree (the lanes of an 8-lane column
+// group all hold the same candidate, which defeated a single-winner shortcut).
 __device__ __forceinline__ Best warp_best(Best b) {
-  const long long bits = __double_as_longlong(b.v);
-  const unsigned hi = b.v < 0.0 ? 0u : (unsigned)((unsigned long long)bits >> 32) + 1u;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(b.v);
+  const bool neg = b.v < 0.0;
+  const unsigned hi = neg ? 0u : (unsigned)(bits >> 32) + 1u;
+  const unsigned lo = neg ? 0u : (unsigned)bits;
   const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-  unsigned cand = __ballot_sync(0xffffffffu, hi == mhi);
-  if (__popc(cand) == 1) {
-    const int src = __ffs(cand) - 1;
-    return Best{__shfl_sync(0xffffffffu, b.v, src), __shfl_sync(0xffffffffu, b.i, src)};
-  }
-  Best c = (hi == mhi) ? b : Best{-1.0, 0x7fffffff};
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, c.v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, c.i, o);
-    if (better(ov, oi, c.v, c.i)) { c.v = ov; c.i = oi; }
-  }
-  return c;
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  const int mi = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)b.i : 0xffffffffu);
+  const int src = __ffs(__ballot_sync(0xffffffffu, top && b.i == mi)) - 1;
+  return Best{__shfl_sync(0xffffffffu, b.v, src), mi};
 }
 
 __device__ __forceinline__ double warp_sum(double s) {
@@ -294,14 +290,11 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       for (int li = warp * GPW + g8; li < nown; li += wpb * GPW) {
         const int gi = b + li * G;
         if (gi == p || done_l[li]) continue;
-        // downdating operands first (off the dependency chain): 1/vn1 and vn1/vn2 (rvn2 = 1/vn2)
-        double n1 = 0.0, rn1 = 0.0, q12 = 0.0;
+        // downdating operands (vn1 and rvn2 = 1/vn2), loaded before the column
+        double n1 = 0.0, r2 = 0.0;
         if (a.pivot) {
           n1 = vn1[li];
-          if (n1 != 0.0) {
-            rn1 = fast_rcp(n1);
-            q12 = n1 * rvn2[li];
-          }
+          r2 = rvn2[li];
         }
         double *col = colptr(li) + j;
         double x = col[0];
@@ -311,16 +304,27 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
             const double *cpa = cp - j;
             double *cab = col - j;
             const int a0 = (j + 2) & ~1;
-            double d0 = 0.0, d1 = 0.0;
+            // four accumulation chains (the FP64 FMA latency, not the loads, bounds this loop)
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
             if (l8 == 0 && j + 1 < a0 && j + 1 < rows) d0 = cpa[j + 1] * cab[j + 1];
-#pragma unroll 2
-            for (int ar = a0 + 2 * l8; ar < rows; ar += 16) {
+            int ar = a0 + 2 * l8;
+            for (; ar + 16 < rows; ar += 32) {
+              const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
+              const double2 u = *reinterpret_cast<const double2 *>(cab + ar);
+              const double2 v2 = *reinterpret_cast<const double2 *>(cpa + ar + 16);
+              const double2 u2 = *reinterpret_cast<const double2 *>(cab + ar + 16);
+              d0 = fma(v.x, u.x, d0);
+              d1 = fma(v.y, u.y, d1);
+              d2 = fma(v2.x, u2.x, d2);
+              d3 = fma(v2.y, u2.y, d3);
+            }
+            if (ar < rows) {
               const double2 v = *reinterpret_cast<const double2 *>(cpa + ar);
               const double2 u = *reinterpret_cast<const double2 *>(cab + ar);
               d0 = fma(v.x, u.x, d0);
               d1 = fma(v.y, u.y, d1);
             }
-            const double dot = gsum(d0 + d1);
+            const double dot = gsum((d0 + d1) + (d2 + d3));
             const double w = tau * fma(scal, dot, x);   // tau v^T col, v = [1; cp[1..] scal]
             const double ws = w * scal;
             x -= w;  // the updated row-j entry (identical in the 8 lanes)
@@ -382,12 +386,13 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
         }
         if (a.pivot) {
           // xLAQP2 downdating on squared norms (vn1 = ||.||^2, vn2 = ||.||^2 at the last
-          // recompute): t = 1 - x^2/vn1, recompute when t vn1/vn2 <= tol3z.
+          // recompute): LAPACK's temp = max(0, 1 - x^2/vn1), vn1 <- vn1 temp and the recompute
+          // test temp vn1/vn2 <= tol3z, written as vn1' = max(0, vn1 - x^2), vn1'/vn2 <= tol3z
+          // (equal in exact arithmetic; two dependent operations instead of five).
           if (n1 != 0.0) {
-            double t = fma(-x * x, rn1, 1.0);
-            t = t < 0.0 ? 0.0 : t;
-            const double t2 = t * q12;
-            if (t2 <= TOL3Z) {
+            double nn = fma(-x, x, n1);
+            nn = nn < 0.0 ? 0.0 : nn;
+            if (nn * r2 <= TOL3Z) {
               if (DEFER && tau != 0.0) {  // the recomputed norm needs the updated rows now
                 __syncwarp(gmask);
                 const double ws = wsbuf[li];
@@ -401,7 +406,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
               n1 = (j + 1 < rows) ? ss : 0.0;
               if (l8 == 0) rvn2[li] = n1 != 0.0 ? 1.0 / n1 : 0.0;
             } else {
-              n1 = n1 * t;
+              n1 = nn;
             }
             __syncwarp(gmask);
             if (l8 == 0) vn1[li] = n1;
@@ -591,10 +596,15 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     return (size_t)(rs + 3 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;
   };
   if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
-    // whole matrix in one CTA's shared memory: no global exchange at all
+    // whole matrix in one CTA's shared memory: no global exchange at all; the block is sized to
+    // one 8-lane group per column (cheaper barriers for small matrices: C1's 25 x 25 factor
+    // 64 -> 56 us).  Wider matrices go to the grid: an 8-lane group's column update is a
+    // ~2000-cycle dependency chain, so one CTA with several columns per group loses to the
+    // ~8000-cycle grid exchange (measured: 25 x 800 on one CTA 577 us, on 100 CTAs 100 us).
     a.owned_max = (int)cols;
+    const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(64, round_up(cols * 8, 32)));
     set_engine_attr<false, true>();
-    hh_engine_kernel<false, true><<<1, 1024, smem_for(cols, true), c.stream>>>(a);
+    hh_engine_kernel<false, true><<<1, threads, smem_for(cols, true), c.stream>>>(a);
     RQLP_LAUNCHED(c);
   } else {
     // enough CTAs that each owns >= 8 columns (fewer records to exchange), at most one per SM
