@@ -106,6 +106,9 @@ class Handle:
             return cls._cache[key]
 
     def workspace(self, variant, m, n, k, p, q, d, b):
+        key = (variant, m, n, k, p, q, d, b or 0)
+        if key == getattr(self, "_ws_key", None):   # same problem, workspace already attached
+            return
         sz = ctypes.c_size_t()
         _check(lib().rqlp_workspace_size(self.h, variant, m, n, k, p, q, d, b or 0, ctypes.byref(sz)),
                "rqlp_workspace_size")
@@ -115,8 +118,10 @@ class Handle:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         _check(lib().rqlp_set_workspace(self.h, ctypes.c_void_p(self._ws.data_ptr()), self._ws.numel()),
                "rqlp_set_workspace")
+        self._ws_key = key
 
     def clear_workspace(self):
+        self._ws_key = None
         _check(lib().rqlp_set_workspace(self.h, None, 0), "rqlp_set_workspace")
 
     def sync(self) -> int:
@@ -157,6 +162,19 @@ def _handle(handle):
     return handle if handle is not None else Handle.default()
 
 
+def _outputs(m: int, n: int, l: int, npiv: int, device):
+    """Q (m x l), T (l x l), P (n x l) column-major and `npiv` int64 pivot vectors of length l,
+    carved from ONE allocation (a call's host cost is dominated by allocations at small sizes)."""
+    tot = (m + l + n + npiv) * l
+    buf = torch.empty(tot, dtype=torch.float64, device=device)
+    out = [buf.as_strided((m, l), (1, m), 0), buf.as_strided((l, l), (1, l), m * l),
+           buf.as_strided((n, l), (1, n), (m + l) * l)]
+    if npiv:
+        bi = buf.view(torch.int64)
+        out += [bi.as_strided((l,), (1,), (m + l + n + i) * l) for i in range(npiv)]
+    return out
+
+
 # ------------------------------------------------------------------ factorisations
 def rqlp(A: torch.Tensor, k: int, p: int, q: int = 0, seed: int = 0, handle: Handle | None = None):
     """RQLP (Alg. 1) + q subspace iterations.  Returns Q (m x l), L (l x l lower),
@@ -166,9 +184,7 @@ def rqlp(A: torch.Tensor, k: int, p: int, q: int = 0, seed: int = 0, handle: Han
     m, n = A.shape
     l = k + p
     h.workspace(VARIANT_RQLP, m, n, k, p, q, 0, 0)
-    Q, L, P = cm_empty(m, l, A.device), cm_empty(l, l, A.device), cm_empty(n, l, A.device)
-    piv0 = torch.empty(l, dtype=torch.int64, device=A.device)
-    piv1 = torch.empty(l, dtype=torch.int64, device=A.device)
+    Q, L, P, piv0, piv1 = _outputs(m, n, l, 2, A.device)
     _check(lib().rqlp_ex(h.h, m, n, k, p, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
                          _ptr(piv0), _ptr(piv1)), "rqlp_ex")
     return Q, L, P, piv0, piv1
@@ -182,8 +198,7 @@ def erqlp(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 2, seed: int = 0
     m, n = A.shape
     l = k + p
     h.workspace(VARIANT_ERQLP, m, n, k, p, q, d, 0)
-    Q, T, P = cm_empty(m, l, A.device), cm_empty(l, l, A.device), cm_empty(n, l, A.device)
-    piv0 = torch.empty(l, dtype=torch.int64, device=A.device)
+    Q, T, P, piv0 = _outputs(m, n, l, 1, A.device)
     tu = ctypes.c_int(0)
     _check(lib().erqlp_ex(h.h, m, n, k, p, q, d, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(T), _ld(T),
                           ctypes.byref(tu), _ptr(P), _ld(P), _ptr(piv0)), "erqlp_ex")
@@ -197,9 +212,7 @@ def brqlp(A: torch.Tensor, k: int, p: int, b: int, q: int = 0, seed: int = 0, ha
     m, n = A.shape
     l = k + p
     h.workspace(VARIANT_BRQLP, m, n, k, p, q, 0, b)
-    Q, L, P = cm_empty(m, l, A.device), cm_empty(l, l, A.device), cm_empty(n, l, A.device)
-    piv0 = torch.empty(l, dtype=torch.int64, device=A.device)
-    piv1 = torch.empty(l, dtype=torch.int64, device=A.device)
+    Q, L, P, piv0, piv1 = _outputs(m, n, l, 2, A.device)
     _check(lib().brqlp_ex(h.h, m, n, k, p, b, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P),
                           _ld(P), _ptr(piv0), _ptr(piv1)), "brqlp_ex")
     return Q, L, P, piv0, piv1

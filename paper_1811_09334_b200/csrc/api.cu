@@ -8,6 +8,8 @@
 
 #include "internal.cuh"
 
+#include <tuple>
+
 struct rqlp_handle_s {
   int magic = 0x51504c52;
   int device = 0;
@@ -43,7 +45,6 @@ struct rqlp_handle_s {
   std::map<std::string, GEntry> graphs;
   std::map<std::string, int> seen;
   cudaStream_t gstream = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaStream_t side = nullptr;  // Ctx::branch() stream and its fork/join events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
@@ -138,8 +139,7 @@ bool graphs_enabled(rqlp_handle_t h) {
 }
 
 // Run `enqueue(Ctx&)` eagerly on the handle's stream, or -- from the second call with the same
-// key -- as a captured CUDA graph replayed on a handle-owned stream that is fenced to the caller's
-// stream with events (so the call stays asynchronous and stream-ordered for the caller).
+// key -- as a CUDA graph captured on a handle-owned stream and replayed on the handle's stream.
 template <typename F>
 int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
   if (!graphs_enabled(h)) {
@@ -159,8 +159,6 @@ int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
   }
   if (!h->gstream) {
     RQLP_CUDA(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
-    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
-    RQLP_CUDA(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   }
   if (it == h->graphs.end()) {
     rqlp_handle_s::GEntry e;
@@ -193,30 +191,28 @@ int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
     }
     it = h->graphs.emplace(key, std::move(e)).first;
   }
-  RQLP_CUDA(cudaEventRecord(h->ev_in, h->stream));
-  RQLP_CUDA(cudaStreamWaitEvent(h->gstream, h->ev_in, 0));
-  RQLP_CUDA(cudaGraphLaunch(it->second.exec, h->gstream));
-  RQLP_CUDA(cudaEventRecord(h->ev_out, h->gstream));
-  RQLP_CUDA(cudaStreamWaitEvent(h->stream, h->ev_out, 0));
+  // captured on the handle's private stream (the caller's may be the legacy default stream, which
+  // cannot capture); replayed directly on the caller's stream (stream-ordered, no event fences)
+  RQLP_CUDA(cudaGraphLaunch(it->second.exec, h->stream));
   h->cur_events = &it->second.events;
   h->launches = it->second.launches;
   return RQLP_OK;
 }
 
+// Graph-cache key: the tag, then the raw bytes of every integer and pointer argument, the timing
+// switch and the stream (binary: no formatting on the per-call path).
 std::string make_key(rqlp_handle_t h, const char *tag, std::initializer_list<int64_t> ints,
                      std::initializer_list<const void *> ptrs) {
   std::string k = tag;
-  char buf[40];
-  for (int64_t v : ints) {
-    snprintf(buf, sizeof buf, ",%lld", (long long)v);
-    k += buf;
-  }
-  for (const void *p : ptrs) {
-    snprintf(buf, sizeof buf, ",%p", p);
-    k += buf;
-  }
-  snprintf(buf, sizeof buf, ",t%d,s%p", h->timing ? 1 : 0, (void *)h->stream);
-  k += buf;
+  k.reserve(k.size() + 1 + 8 * (ints.size() + ptrs.size() + 2));
+  k += '\0';
+  auto put = [&](const void *p, size_t n) { k.append(reinterpret_cast<const char *>(p), n); };
+  for (int64_t v : ints) put(&v, sizeof v);
+  for (const void *p : ptrs) put(&p, sizeof p);
+  const int64_t t = h->timing ? 1 : 0;
+  put(&t, sizeof t);
+  const void *st = (const void *)h->stream;
+  put(&st, sizeof st);
   return k;
 }
 
@@ -259,10 +255,21 @@ void carve_plan(Arena &a, Plan &p, int variant, int64_t m, int64_t n, int64_t l,
 }
 
 size_t plan_bytes(int variant, int64_t m, int64_t n, int64_t l, int b, int num_sms) {
+  // memoised: the measuring carve runs the GEMM split models of every pass (host cost per call)
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int>, size_t> memo;
+  const auto key = std::make_tuple(variant, m, n, l, b, num_sms);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
   Arena a;
   Plan p;
   carve_plan(a, p, variant, m, n, l, b, num_sms);
-  return a.used + 4096;
+  std::lock_guard<std::mutex> g(mu);
+  if (memo.size() > 256) memo.clear();
+  return memo[key] = a.used + 4096;
 }
 
 // Workspace for a call: the caller's if set and large enough, else a library-owned buffer.
@@ -669,8 +676,6 @@ int rqlp_destroy(rqlp_handle_t h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
-  if (h->ev_in) cudaEventDestroy(h->ev_in);
-  if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->own) cudaFree(h->own);
   if (h->stage) cudaFree(h->stage);
   if (h->dflags) cudaFree(h->dflags);

@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         }
       return;
     }
+    // declined: the full factorisation follows; marked (shift_bit << 16 = pass_bit << 24, as the
+    // blocked path's near_identity_kernel does) for callers that iterate until a pass accepts
+    if (tid == 0) atomicOr(shift_word, shift_bit << 16);
   }
   if (tid == 0) { s_fail = 0; s_dep = 0; s_tiny = 0; }
   __syncthreads();
@@ -233,11 +236,12 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         auto tile = [&](int t) {
           int Tr, Tc;
           double a0, a1;
-          if (t < n_s) {  // S tile: enumerate (Tr, Tc) with kb < Tc <= Tr
-            int u = t, cnum = 0;
-            while (u >= ntrail - cnum) { u -= ntrail - cnum; ++cnum; }
-            Tc = kb + 1 + cnum;
-            Tr = Tc + u;
+          if (t < n_s) {  // S tile: (Tr, Tc) with kb < Tc <= Tr, t = rr (rr + 1) / 2 + cr row-major
+            int rr = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+            if ((rr + 1) * (rr + 2) / 2 <= t) ++rr;  // float rounding guards (t < 8256)
+            if (rr * (rr + 1) / 2 > t) --rr;
+            Tr = kb + 1 + rr;
+            Tc = kb + 1 + (t - rr * (rr + 1) / 2);
             const int r = Tr * 8 + fr;
             a0 = M[r + (k0 + 2 * fq) * CB_LD] * dv0;  // L_rK = P_rK Δ^-1
             a1 = M[r + (k0 + 2 * fq + 1) * CB_LD] * dv1;
@@ -525,6 +529,42 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   RQLP_LAUNCHED(c);
 }
 
+__global__ void or_flag_kernel(unsigned *word, unsigned bits) { atomicOr(word, bits); }
+
+// The rare branch for row-sharded orth (orth_rescue.cu's algorithm with allreduced Grams, driven
+// from the host): if the COND word holds one of `mask`'s bits, CholeskyQR passes (shifted on
+// breakdown; zero or, from the 4th pass, numerically dependent columns completed) on V until a
+// pass's Gram is near the identity, then R = V^T Y (allreduced; R's strictly lower part is then
+// rounding noise, not zero).  Reads the COND word back (one stream synchronisation per orth).
+static void sharded_rescue(Ctx &c, OrthScratch &s, int64_t m, int64_t n, double *V, int64_t ldv, const double *Y,
+                           int64_t ldy, double *R, int64_t ldr, unsigned mask) {
+  unsigned *condw = c.dflags + COND_WORD;
+  unsigned host = 0;
+  RQLP_CUDA(cudaMemcpyAsync(&host, condw, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
+  RQLP_CUDA(cudaStreamSynchronize(c.stream));
+  if (!(host & mask)) return;
+  const int64_t lc = round_up(n, 8);
+  double *cur = V, *nxt = s.Ybuf;
+  int64_t ldc = ldv, ldn = s.ldy;
+  for (int pass = 0; pass < 10; ++pass) {
+    RQLP_CUDA(cudaMemsetAsync(condw, 0, sizeof(unsigned), c.stream));
+    cholqr_pass(c, s, m, n, cur, ldc, nxt, ldn, s.R, 4u, nullptr, 0, true, true, pass >= 3);
+    std::swap(cur, nxt);
+    std::swap(ldc, ldn);
+    RQLP_CUDA(cudaMemcpyAsync(&host, condw, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
+    RQLP_CUDA(cudaStreamSynchronize(c.stream));
+    if (!(host & (4u << 24))) break;  // this pass's Gram was near the identity: cur is orthonormal
+  }
+  if (cur != V) launch_copy(c, m, n, cur, ldc, V, ldv, false);
+  if (R) {
+    gemm_tn(c, m, n, n, V, ldv, Y, ldy, s.tmp, lc, false, s.partials, s.partial_elems);
+    allreduce_sum(c, s.tmp, lc * n);
+    launch_copy(c, n, n, s.tmp, lc, R, ldr, false);
+  }
+  or_flag_kernel<<<1, 1, 0, c.stream>>>(c.dflags + FLAG_WORD, (unsigned)RQLP_FLAG_SHIFTED_CHOLQR);
+  RQLP_LAUNCHED(c);
+}
+
 void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t ldy, double *V, int64_t ldv,
           double *R, int64_t ldr, bool sharded, bool span_only) {
   int64_t lc = round_up(n, 8);
@@ -541,7 +581,8 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
       launch_orth_rescue(c, s, m, n, V, ldv, Y, ldy, nullptr, 0, condw, 1u << 8);
       return;
     }
-    cholqr_pass(c, s, m, n, Y, ldy, V, ldv, s.Racc, 1u, nullptr, 0, sharded);
+    cholqr_pass(c, s, m, n, Y, ldy, V, ldv, s.Racc, 1u, nullptr, 0, true, false, false);
+    sharded_rescue(c, s, m, n, V, ldv, Y, ldy, nullptr, 0, 1u << 8);
     return;
   }
   // pass 1: Y -> Ybuf (R1 in Racc), pass 2: Ybuf -> V (R2 in R)
@@ -555,25 +596,13 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
     launch_orth_rescue(c, s, m, n, V, ldv, Y, ldy, R, ldr, condw, (1u << 8) | (2u << 8));
     return;
   }
-  // row-sharded: the Gram is an allreduce, so the rare branch stays a conditional third pass
-  cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, sharded);
-  cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, sharded, true);
+  // row-sharded (eager only: graphs are off with a communicator): CholeskyQR2 as above, the rare
+  // branch driven from the host -- every rank reads the same COND word (the Grams are allreduced,
+  // so every rank takes the same decisions) and runs the same extra passes
+  cholqr_pass(c, s, m, n, Y, ldy, s.Ybuf, s.ldy, s.Racc, 1u, nullptr, 0, true, false, false);
+  cholqr_pass(c, s, m, n, s.Ybuf, s.ldy, V, ldv, s.R, 2u, nullptr, 0, true, true, false);
   if (R) gemm_nn(c, n, n, n, s.R, lc, s.Racc, lc, R, ldr, s.partials, s.partial_elems);  // R = R2 R1
-  // pass 3 (only when pass 1 or 2 needed the shift, bits 1<<8 | 2<<8, or completed dependent
-  // columns, bits 1<<16 | 2<<16): V -> Ybuf -> V
-  const unsigned m3 = (1u << 8) | (2u << 8) | (1u << 16) | (2u << 16);
-  cholqr_pass(c, s, m, n, V, ldv, s.Ybuf, s.ldy, s.R, 4u, condw, m3, sharded, true);
-  launch_copy(c, m, n, s.Ybuf, s.ldy, V, ldv, false, condw, m3);
-  if (R) {
-    gemm_nn(c, n, n, n, s.R, lc, R, ldr, s.tmp, lc, s.partials, s.partial_elems, condw, m3);  // R3 R2 R1
-    launch_copy(c, n, n, s.tmp, lc, R, ldr, false, condw, m3);
-    // with completed columns Y = V R no longer holds for R2 R1: R = V^T Y (upper triangular in
-    // exact arithmetic, zero rows for the completed directions)
-    const unsigned mdep = (1u << 16) | (2u << 16) | (4u << 16);
-    gemm_tn(c, m, n, n, V, ldv, Y, ldy, s.tmp, lc, false, s.partials, s.partial_elems, condw, mdep);
-    if (sharded) allreduce_sum(c, s.tmp, lc * n);
-    launch_copy(c, n, n, s.tmp, lc, R, ldr, false, condw, mdep);
-  }
+  sharded_rescue(c, s, m, n, V, ldv, Y, ldy, R, ldr, (1u << 8) | (2u << 8));
 }
 
 }  // namespace rqlpk

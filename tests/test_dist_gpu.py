@@ -53,3 +53,38 @@ def test_nccl_world1_bit_identical(world1, variant):
     torch.cuda.synchronize()
     for key in ("Q", "T", "P", "piv0"):
         assert torch.equal(g0[key], g1[key]), key
+
+
+@pytest.mark.parametrize("kind", ["illcond", "deficient", "zero"])
+@pytest.mark.parametrize("d", [0, 2])
+def test_nccl_world1_rare_branch(world1, kind, d):
+    """Sketches beyond CholeskyQR2's reach on the row-sharded path: its host-driven shifted passes
+    (allreduced Grams) must give an orthonormal Q and the residual of the single-GPU handle
+    (whose rescue is one cooperative kernel -- same algorithm, different reduction order)."""
+    dist = world1
+    import oracle as orc
+
+    import paper_1811_09334_b200 as rq
+    rng = np.random.default_rng(11)
+    m, n = 600, 400
+    sig = {"illcond": np.logspace(0, -13, 16), "deficient": np.array([3.0, 2.0, 1.0, 0.5, 0.25, 0.125]),
+           "zero": np.zeros(4)}[kind]
+    U, _ = np.linalg.qr(rng.standard_normal((m, len(sig))))
+    V, _ = np.linalg.qr(rng.standard_normal((n, len(sig))))
+    A_np = np.asfortranarray((U * sig) @ V.T)
+    A = torch.from_numpy(np.ascontiguousarray(A_np.T)).cuda().t()
+    hd = rq.Handle(group=dist.group.WORLD)
+    g1 = rq.factorize(A, 12, 4, q=1, d=d, seed=5, handle=hd)
+    flags = hd.sync()
+    g0 = rq.factorize(A, 12, 4, q=1, d=d, seed=5, handle=rq.Handle())
+    torch.cuda.synchronize()
+    Q1, T1, P1 = (np.asfortranarray(g1[k].cpu().numpy()) for k in ("Q", "T", "P"))
+    Q0, T0, P0 = (np.asfortranarray(g0[k].cpu().numpy()) for k in ("Q", "T", "P"))
+    assert np.abs(Q1.T @ Q1 - np.eye(16)).max() <= 1e-13 * 16
+    assert np.abs(P1.T @ P1 - np.eye(16)).max() <= 1e-13 * 16
+    r1, r0 = orc.residual(A_np, Q1, T1, P1), orc.residual(A_np, Q0, T0, P0)
+    assert r1 <= 10 * r0 + 1e-13 * max(np.linalg.norm(A_np), 1.0)
+    assert flags & 1  # the shifted passes ran
+    k = len(sig) if kind != "illcond" else 6
+    if kind != "zero":
+        np.testing.assert_allclose(np.abs(np.diag(T1))[:k], np.abs(np.diag(T0))[:k], rtol=1e-8)
