@@ -248,29 +248,57 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
 }
 
 // Sum of a balanced split's slots: element (i, j) of tile t = (i / BM) ntn + j / bn is the sum,
-// in slot order, of the partial tiles of the CTAs first(t) .. last(t) whose runs touch t.
-__global__ void bal_reduce_kernel(int M, int N, int bn, int ntn, int ktiles, int units, int maxc,
-                                  const double *__restrict__ part, double *__restrict__ C, int64_t ldc, int trans,
-                                  const unsigned *cond, unsigned cond_mask) {
+// in slot order, of the partial tiles of the CTAs first(t) .. last(t) whose runs touch t.  A CTA
+// reduces a 32 x 32 block (threads along i: coalesced slot reads); the transposed store goes
+// through shared memory so it is coalesced along j.
+__global__ void __launch_bounds__(256) bal_reduce_kernel(int M, int N, int bn, int ntn, int ktiles, int units,
+                                                         int maxc, const double *__restrict__ part,
+                                                         double *__restrict__ C, int64_t ldc, int trans,
+                                                         const unsigned *cond, unsigned cond_mask) {
   if (cond && ((*cond) & cond_mask) == 0) return;
-  const int64_t total = (int64_t)M * N;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int i, j;
-    if (trans) {  // consecutive threads along j: coalesced stores into C^T
-      i = (int)(e / N);
-      j = (int)(e % N);
-    } else {
-      i = (int)(e % M);
-      j = (int)(e / M);
+  __shared__ double sm[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int nbi = (M + 31) / 32, nbj = (N + 31) / 32;
+  for (int blk = blockIdx.x; blk < nbi * nbj; blk += gridDim.x) {
+    const int i0 = (blk % nbi) * 32, j0 = (blk / nbi) * 32;
+    const int i = i0 + tx;
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int j = j0 + jj;
+      double sum = 0.0;
+      if (i < M && j < N) {
+        const int mt = i / BM, nt = j / bn, t = mt * ntn + nt;
+        const int first = (int)(((long long)t * ktiles) / units);
+        const int last = (int)(((long long)(t + 1) * ktiles - 1) / units);
+        const double *p = part + (size_t)t * maxc * (BM * bn) + (i - mt * BM) + (size_t)(j - nt * bn) * BM;
+        const int cnt = last - first + 1;
+        // all slot loads in flight first (memory-level parallelism), then the ordered sum
+        int q = 0;
+        for (; q + 8 <= cnt; q += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = p[(size_t)(q + u) * (BM * bn)];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = q + u < cnt ? p[(size_t)(q + u) * (BM * bn)] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q + u < cnt) sum += v[u];
+        if (!trans) C[i + (int64_t)j * ldc] = sum;
+      }
+      sm[jj][tx] = sum;
     }
-    const int mt = i / BM, nt = j / bn, t = mt * ntn + nt;
-    const int first = (int)(((long long)t * ktiles) / units);
-    const int last = (int)(((long long)(t + 1) * ktiles - 1) / units);
-    const double *p = part + (size_t)t * maxc * (BM * bn) + (i - mt * BM) + (size_t)(j - nt * bn) * BM;
-    double sum = 0.0;
-    for (int q = 0; q <= last - first; ++q) sum += p[(size_t)q * (BM * bn)];
-    if (trans) C[j + (int64_t)i * ldc] = sum;
-    else C[i + (int64_t)j * ldc] = sum;
+    if (trans) {
+      __syncthreads();
+      const int j = j0 + tx;
+      for (int ii = ty; ii < 32; ii += 8) {
+        const int ir = i0 + ii;
+        if (ir < M && j < N) C[j + (int64_t)ir * ldc] = sm[tx][ii];
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -398,7 +426,7 @@ void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int 
     gemm_tma_kernel<BN, MODE><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
                                                                      part, cond, mask, 0, bp.units, ntn, bp.maxc);
     RQLP_LAUNCHED(c);
-    const int grid = (int)std::min<int64_t>(ceil_div((int64_t)M * N, 256), (int64_t)c.num_sms * 16);
+    const int grid = (int)std::min<int64_t>(ceil_div(M, 32) * ceil_div(N, 32), (int64_t)c.num_sms * 8);
     bal_reduce_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(M, N, BN, ntn, ktiles, bp.units, bp.maxc, part, C, ldc,
                                                                 trans ? 1 : 0, cond, mask);
     RQLP_LAUNCHED(c);
