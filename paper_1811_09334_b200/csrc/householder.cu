@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
   __shared__ double s_bv[2][32];
   __shared__ int s_bi[2][32];
   __shared__ int s_p;
+  __shared__ double s_xn2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const int G = GRID ? (int)gridDim.x : 1, b = GRID ? (int)blockIdx.x : 0;
   const int nown = b < a.cols ? (a.cols - b + G - 1) / G : 0;  // columns b, b+G, b+2G, ...
@@ -146,10 +147,18 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
     else if (jn < a.cols && jn % G == b) src = jn;
     if (src >= 0) {
       const double *sp = colptr((src - b) / G);
-      unsigned long long *dst = a.cand + ((int64_t)par * G + b) * rows * 2;
+      unsigned long long *dst = a.cand + ((int64_t)par * G + b) * (rows + 1) * 2;
+      double s2 = 0.0;  // sum of squares of rows jn+1..: the next reflector's xnorm^2, computed once
       for (int r = jn + lane; r < rows; r += 32) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(sp[r]);
+        const double v = sp[r];
+        if (r > jn) s2 = fma(v, v, s2);
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
         st_x2(dst + 2 * (r - jn), pack((unsigned)bits, tag), pack((unsigned)(bits >> 32), tag));
+      }
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(s2);
+        st_x2(dst + 2 * (rows - jn), pack((unsigned)bits, tag), pack((unsigned)(bits >> 32), tag));
       }
     }
     if (lane == 0 && (a.pivot || src >= 0)) {
@@ -235,13 +244,15 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       }
       __syncthreads();
       p = s_p;
-      const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * rows * 2;
-      for (int r = threadIdx.x; r < len; r += blockDim.x) {
+      const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * (rows + 1) * 2;
+      for (int r = threadIdx.x; r <= len; r += blockDim.x) {  // r == len: the published xnorm^2
         unsigned long long lo, hi;
         do {
           ld_x2(src + 2 * r, lo, hi);
         } while ((unsigned)lo != tag || (unsigned)hi != tag);
-        vraw[j + r] = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
+        const double v = __longlong_as_double((long long)(((hi >> 32) << 32) | (lo >> 32)));
+        if (r < len) vraw[j + r] = v;
+        else s_xn2 = v;
       }
       __syncthreads();
       cp = vraw + j;
@@ -251,10 +262,16 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
     }
     stamp(1);
 
-    // ---- reflector (xLARFG), recomputed by every warp with the same order -> identical bits
-    double part = 0.0;
-    for (int r = 1 + lane; r < len; r += 32) part = fma(cp[r], cp[r], part);
-    const double xn2 = warp_sum(part);
+    // ---- reflector (xLARFG), recomputed by every warp from the same values -> identical bits
+    //      (grid: ||rows j+1..||^2 comes with the candidate, summed once by its publisher)
+    double xn2;
+    if (GRID) {
+      xn2 = s_xn2;
+    } else {
+      double part = 0.0;
+      for (int r = 1 + lane; r < len; r += 32) part = fma(cp[r], cp[r], part);
+      xn2 = warp_sum(part);
+    }
     const double alpha = cp[0];
     double tau, beta, scal;
     if (xn2 == 0.0) {
@@ -570,7 +587,7 @@ void hh_carve(Arena &a, HHScratch &s, int64_t rows, int64_t cols, int num_sms, i
   s.tau = a.take<double>(steps);
   s.beta = a.take<double>(steps);
   s.rec = a.take<unsigned long long>(2 * s.max_slots * 4);
-  s.cand = a.take<unsigned long long>(2 * s.max_slots * rows * 2);
+  s.cand = a.take<unsigned long long>(2 * s.max_slots * (rows + 1) * 2);
   s.done = a.take<int>(cols);
   s.perm = a.take<int64_t>(cols);
 }
@@ -618,7 +635,7 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     // zero the exchange buffers every launch: tags are then step+1 of THIS launch only (robust
     // against recycled workspaces; a memset node when captured in a CUDA graph)
     RQLP_CUDA(cudaMemsetAsync(s.rec, 0, sizeof(unsigned long long) * 2 * G * 4, c.stream));
-    RQLP_CUDA(cudaMemsetAsync(s.cand, 0, sizeof(unsigned long long) * 2 * G * rows * 2, c.stream));
+    RQLP_CUDA(cudaMemsetAsync(s.cand, 0, sizeof(unsigned long long) * 2 * G * (rows + 1) * 2, c.stream));
     a.epoch = 0;
     // co-residency of all G CTAs is required (they exchange every step): cooperative launch
     // through cudaLaunchKernelEx (capturable into CUDA graphs)
