@@ -74,45 +74,42 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   __shared__ int s_fail, s_dep, s_tiny;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int npad = (n + 7) & ~7, nt = npad >> 3;
-  // M(b, a) = G[a + b ldg] (+ shift on the diagonal) for a <= b: the lower part (read coalesced
-  // over a; a flat unrolled loop keeps many loads in flight -- one CTA streams the whole matrix),
-  // the upper part (the W^T entries) zero, identity padding.  shift > 0: the retry after a
-  // breakdown (shifted CholeskyQR, G + shift I); dep detection is then off.
+  // M = the Gram's lower part (M(r, c) = G[r + c ldg], r >= c; + shift on the diagonal), the upper
+  // part (the W^T entries) zero, identity padding.  The fused path's Gram is formed whole (n <= 128
+  // is one 128-row GEMM tile) and symmetric, as are the blocked path's diagonal blocks, so no
+  // transpose is needed: 16-byte loads and stores along columns (a flat unrolled loop keeps many
+  // loads in flight; transposed stores were 16-way bank conflicts, ~5 us of the kernel).
+  // shift > 0: the retry after a breakdown (shifted CholeskyQR, G + shift I).
   auto load = [&](double shift) {
-    // row pairs (a, a+1) of column b: 16-byte loads when the column start is 16-byte aligned
     const int hp = npad >> 1, tot = hp * npad;
     const bool vec = ((ldg & 1) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
-    // (pair index, column) advanced incrementally: no integer division in the loop
+    // (row pair, column) advanced incrementally: no integer division in the loop
     const int da = blockDim.x % hp, db = blockDim.x / hp;
     int ai = tid % hp, bi = tid / hp;
-#pragma unroll 8
+    // the original diagonal first (its loads overlap the matrix's)
+    for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
+#pragma unroll 16
     for (int e = tid; e < tot; e += blockDim.x) {
-      const int a = 2 * ai, b = bi;
+      const int r = 2 * ai, c = bi;
       ai += da;
       bi += db;
       if (ai >= hp) { ai -= hp; ++bi; }
-      if (a > b) continue;
-      double v0 = (a == b) ? 1.0 : 0.0, v1 = (a + 1 == b) ? 1.0 : 0.0;
-      if (b < n) {
-        const double *src = G + a + (int64_t)b * ldg;  // a + 1 <= npad - 1; rows >= n are unused
-        if (vec && a + 1 < n) {
+      double v0 = (r == c) ? 1.0 : 0.0, v1 = (r + 1 == c) ? 1.0 : 0.0;
+      if (c < n && r + 1 >= c) {
+        const double *src = G + r + (int64_t)c * ldg;
+        if (vec && r + 1 < n) {
           const double2 t = *reinterpret_cast<const double2 *>(src);
-          v0 = t.x; v1 = t.y;
+          if (r >= c) v0 = t.x;
+          v1 = t.y;
         } else {
-          v0 = src[0];
-          v1 = a + 1 < n ? src[1] : v1;
+          if (r >= c && r < n) v0 = src[0];
+          if (r + 1 < n) v1 = src[1];
         }
-        if (a == b) v0 += shift;
-        if (a + 1 == b) v1 += shift;
+        if (r == c) v0 += shift;
+        if (r + 1 == c) v1 += shift;
       }
-      M[b + a * CB_LD] = v0;
-      if (a < b) M[a + b * CB_LD] = 0.0;
-      if (a + 1 <= b) {
-        M[b + (a + 1) * CB_LD] = v1;
-        if (a + 1 < b) M[a + 1 + b * CB_LD] = 0.0;
-      }
+      *reinterpret_cast<double2 *>(M + r + c * CB_LD) = make_double2(v0, v1);
     }
-    for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
   };
   load(0.0);
   __syncthreads();
