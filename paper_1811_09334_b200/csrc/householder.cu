@@ -450,9 +450,36 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
         for (int r = j + 1 + l0; r < rows; r += stride) cab[r] = fma(-ws, cp[r - j], cab[r]);
       };
       if (warp == 0) {
-        if (lbest >= 0 && tau != 0.0) finish(lbest, lane, 32);
-        __syncwarp();
-        if (j + 1 < a.steps) publish(j + 1, cb);
+        const double wsb = (lbest >= 0 && tau != 0.0) ? wsbuf[lbest] : 0.0;
+        if (wsb != 0.0 && j + 1 < a.steps) {
+          // the candidate's deferred update fused with its publish: rows j+1.. updated, stored
+          // back and sent in one pass (plus their sum of squares below row j+1 and the record)
+          const int jn = j + 1, par2 = jn & 1;
+          const unsigned tag = (a.epoch << 16) | ((unsigned)jn + 1u);
+          double *cab = colptr(lbest);
+          unsigned long long *dst = a.cand + ((int64_t)par2 * G + b) * (rows + 1) * 2;
+          double s2 = 0.0;
+          for (int r = jn + lane; r < rows; r += 32) {
+            const double v = fma(-wsb, cp[r - j], cab[r]);
+            cab[r] = v;
+            if (r > jn) s2 = fma(v, v, s2);
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+            st_x2(dst + 2 * (r - jn), pack((unsigned)bits, tag), pack((unsigned)(bits >> 32), tag));
+          }
+          s2 = warp_sum(s2);
+          if (lane == 0) {
+            const unsigned long long sb = (unsigned long long)__double_as_longlong(s2);
+            st_x2(dst + 2 * (rows - jn), pack((unsigned)sb, tag), pack((unsigned)(sb >> 32), tag));
+            const unsigned long long vb = (unsigned long long)__double_as_longlong(cb.v);
+            unsigned long long *rc = a.rec + ((int64_t)par2 * G + b) * 4;
+            st_x2(rc, pack((unsigned)(vb >> 32), tag), pack((unsigned)vb, tag));
+            st_x1(rc + 2, pack((unsigned)cb.i, tag));
+          }
+        } else {
+          if (wsb != 0.0) finish(lbest, lane, 32);
+          __syncwarp();
+          if (j + 1 < a.steps) publish(j + 1, cb);
+        }
       }
       if (tau != 0.0) {
         const int g8 = lane >> 3, l8 = lane & 7;
