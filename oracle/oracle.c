@@ -565,14 +565,19 @@ int orc_rqlp(int64_t m, int64_t n, int k, int p, int q, int d, const double *A, 
   return 0;
 }
 
-/* V_j <- qr(V_j - Vprev (Vprev^T V_j))  (Alg.3 l.5, eq. (18)) */
+/* V_j <- qr(V_j - Vprev (Vprev^T V_j))  (Alg.3 l.5, eq. (18)), applied twice
+ * (reading R28: "twice is enough"; in exact arithmetic the second pass removes nothing
+ * whenever V_j has a component outside span(Vprev), and it is what keeps V orthonormal when that
+ * component is at the rounding level -- a block past rank(A), or past a spectral gap). */
 static void reorth(int64_t m, int64_t nprev, int64_t bj, const double *Vprev, int64_t ldvp, double *Vj) {
   if (nprev == 0) return;
   double *C = dalloc(nprev * bj), *D = dalloc(m * bj), *R = dalloc(bj * bj);
-  orc_gemm_tn(nprev, bj, m, Vprev, ldvp, Vj, m, C, nprev);
-  orc_gemm_nn(m, bj, nprev, Vprev, ldvp, C, nprev, D, m);
-  for (int64_t i = 0; i < m * bj; ++i) D[i] = Vj[i] - D[i];
-  orc_hqr(m, bj, D, m, Vj, m, R, bj);
+  for (int pass = 0; pass < 2; ++pass) {
+    orc_gemm_tn(nprev, bj, m, Vprev, ldvp, Vj, m, C, nprev);
+    orc_gemm_nn(m, bj, nprev, Vprev, ldvp, C, nprev, D, m);
+    for (int64_t i = 0; i < m * bj; ++i) D[i] = Vj[i] - D[i];
+    orc_hqr(m, bj, D, m, Vj, m, R, bj);
+  }
   free(C); free(D); free(R);
 }
 

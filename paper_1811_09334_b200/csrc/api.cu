@@ -441,16 +441,23 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
   // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
+  // Alg.3 l.5, applied twice ("twice is enough", reading R28): identical in exact arithmetic
+  // when V_j has a component outside span(V_<j) (the second projection removes nothing), and
+  // the only way to keep Q orthonormal when it has (almost) none -- a block beyond rank(A), whose
+  // first residual is rounding noise (one pass then returns directions far from orthogonal to
+  // V_<j, as the literal line does in exact arithmetic: qr(0)).
   auto reorth = [&](int64_t c0, int64_t bj) {
     if (c0 == 0) return;
     double *Vj = P.V + c0 * ldm;
     c.mark("b_other");
-    gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
-    allreduce_sum(c, P.C, LL * bj);
-    gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
-                    nullptr, 0);
-    launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
-    orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
+    for (int pass = 0; pass < 2; ++pass) {
+      gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
+      allreduce_sum(c, P.C, LL * bj);
+      gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
+                      nullptr, 0);
+      launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
+      orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
+    }
   };
   // q = 0 (NEXT-4): the range finder needs no A-pass per block, so every V_j is built first
   // and ONE batched pass B = V^T A replaces the h per-block projections; the deflation

@@ -1,0 +1,95 @@
+"""Seeded randomized sweep of the whole factorisation against the oracle: shapes (tall, wide,
+square, ragged against every tile size), k, p, q, d, b and spectra (polynomial, exponential,
+gapped, numerically rank-deficient, exactly rank-deficient) drawn from a fixed seed.  Every case
+checks the north_star tolerances where they are well defined and the basis-invariant quantities
+(residual, orthonormality) everywhere (readings R4, R26)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1811_09334_b200 as rq
+    return rq
+
+
+def _cm(a):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64).T)).cuda().t()
+
+
+def _np(t):
+    return np.asfortranarray(t.detach().cpu().numpy())
+
+
+def _case(i):
+    rng = np.random.default_rng(1000 + i)
+    k = int(rng.integers(2, 40))
+    p = int(rng.integers(2, 12))
+    l = k + p
+    m = int(rng.integers(l, 900))
+    n = int(rng.integers(l, 700))
+    q = int(rng.integers(0, 3))
+    variant = ["rqlp", "erqlp", "brqlp"][int(rng.integers(0, 3))]
+    d = int(rng.integers(1, 5)) if variant == "erqlp" else 0
+    b = int(rng.integers(1, l + 1)) if variant == "brqlp" else None
+    kind = ["poly", "exp", "gap", "numdef", "exactdef"][int(rng.integers(0, 5))]
+    r = min(m, n)
+    j = np.arange(1, r + 1.0)
+    if kind == "poly":
+        sig = j ** -float(rng.uniform(0.5, 2.5))
+    elif kind == "exp":
+        sig = np.exp(-j / float(rng.uniform(3, 60)))
+    elif kind == "gap":
+        sig = np.where(j <= k, 1.0, 1e-6) * j ** -1.0
+    elif kind == "numdef":
+        sig = np.where(j <= max(2, l // 2), j ** -1.0, 1e-17)
+    else:
+        sig = np.where(j <= max(2, l // 2), j ** -1.0, 0.0)
+    U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    A = np.asfortranarray((U * sig) @ V.T)
+    return dict(m=m, n=n, k=k, p=p, q=q, d=d, b=b, variant=variant, kind=kind, A=A, sig=sig, seed=int(rng.integers(0, 2**62)))
+
+
+@pytest.mark.parametrize("i", range(96))
+def test_random_sweep(rq, orc, i):
+    c = _case(i)
+    A, l = c["A"], c["k"] + c["p"]
+    g = rq.factorize(_cm(A), c["k"], c["p"], q=c["q"], d=c["d"], b=c["b"], seed=c["seed"])
+    if c["variant"] == "brqlp":
+        o = orc.brqlp(A, c["k"], c["p"], b=c["b"], q=c["q"], seed=c["seed"])
+    else:
+        o = orc.rqlp(A, c["k"], c["p"], q=c["q"], d=c["d"], seed=c["seed"])
+    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+    nA = np.linalg.norm(A)
+    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+    tag = f"case {i}: {c['variant']} m={c['m']} n={c['n']} k={c['k']} p={c['p']} q={c['q']} d={c['d']} b={c['b']} {c['kind']}"
+    # basis-invariant: orthonormal factors, the oracle's residual (to 1e-12, or relative to it when
+    # the sketch is numerically rank deficient and the completion directions differ)
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
+    if c["variant"] != "brqlp":   # BRQLP's P is orthonormal per block only (reading R17)
+        assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
+    assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
+    # pivots and L-values where they are unique: full-rank sketch with separated leading values
+    rank = int((c["sig"] > 1e-14 * c["sig"][0]).sum())
+    if rank >= l and c["kind"] in ("poly", "exp", "gap"):
+        piv_g = g["piv0"].cpu().numpy()
+        if np.array_equal(piv_g, o["piv0"]):
+            # relative 1e-10 (north_star) where the L-value is above 1e-4 of the largest -- every
+            # L-value of C1-C5 (sigma_l/sigma_1 >= 2.9e-5); below that the achievable agreement
+            # of two FP64 computations is absolute, ~u ||A|| (gapped spectra reach 1e-7 relative)
+            Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
+            big = Lo >= 1e-4 * Lo.max()
+            rel = np.abs(Lg - Lo)[big] / Lo[big]
+            assert rel.max() <= 1e-10, (tag, rel.max())
+            assert np.abs(Lg - Lo).max() <= 1e-13 * Lo.max(), tag
+        else:
+            # a flip is possible only at a numerical near-tie of candidate norms;
+            # the residual already agreed above -- report the step instead of passing silently
+            first = int(np.argmax(piv_g != o["piv0"]))
+            pytest.xfail(f"{tag}: pivot sequences differ from step {first}")
