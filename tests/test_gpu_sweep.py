@@ -93,3 +93,96 @@ def test_random_sweep(rq, orc, i):
             # the residual already agreed above -- report the step instead of passing silently
             first = int(np.argmax(piv_g != o["piv0"]))
             pytest.xfail(f"{tag}: pivot sequences differ from step {first}")
+
+
+def _spectrum(rng, r, k, l):
+    j = np.arange(1, r + 1.0)
+    kind = ["poly", "exp", "gap", "numdef"][int(rng.integers(0, 4))]
+    if kind == "poly":
+        return kind, j ** -float(rng.uniform(0.5, 2.0))
+    if kind == "exp":
+        return kind, np.exp(-j / float(rng.uniform(10, 80)))
+    if kind == "gap":
+        return kind, np.where(j <= k, 1.0, 1e-6) * j ** -1.0
+    return kind, np.where(j <= max(2, l // 2), j ** -1.0, 1e-17)
+
+
+def _rand_A(rng, m, n, sig):
+    r = len(sig)
+    U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return np.asfortranarray((U * sig) @ V.T)
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_sweep_large(rq, orc, i):
+    """Larger shapes (multi-tile GEMMs: split-K and the balanced split, the grid-mode CPQR engine
+    with several columns per CTA, the blocked Cholesky for l > 128)."""
+    rng = np.random.default_rng(5000 + i)
+    k = int(rng.integers(20, 200))
+    p = int(rng.integers(2, 16))
+    l = k + p
+    m = int(rng.integers(max(l, 1500), 4200))
+    n = int(rng.integers(max(l, 1200), 3600))
+    q = int(rng.integers(0, 2))
+    d = int(rng.integers(0, 3))
+    kind, sig = _spectrum(rng, min(m, n, 3 * l), k, l)
+    A = _rand_A(rng, m, n, sig)
+    seed = int(rng.integers(0, 2**62))
+    g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=seed)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=seed)
+    tag = f"large {i}: m={m} n={n} k={k} p={p} q={q} d={d} {kind}"
+    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+    nA = np.linalg.norm(A)
+    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
+    assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
+    assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
+    if kind != "numdef":
+        assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
+        Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
+        big = Lo >= 1e-4 * Lo.max()
+        assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
+        assert np.abs(Lg - Lo).max() <= 1e-13 * Lo.max(), tag
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_sweep_autorank_tqlp(rq, orc, i):
+    """Auto-rank RQLP (NEXT-1) and the truncated QLP (NEXT-3) on random shapes."""
+    rng = np.random.default_rng(9000 + i)
+    m = int(rng.integers(60, 900))
+    n = int(rng.integers(60, 700))
+    kind, sig = _spectrum(rng, min(m, n), 20, 40)
+    A = _rand_A(rng, m, n, sig)
+    nA = np.linalg.norm(A)
+    if i % 2 == 0:
+        b = int(rng.integers(1, 24))
+        l_max = int(rng.integers(b, min(m, n) + 1))
+        eps = float(10 ** rng.uniform(-6, -1))
+        q = int(rng.integers(0, 3))
+        seed = int(rng.integers(0, 2**62))
+        g = rq.autorank(_cm(A), b=b, l_max=l_max, eps=eps, q=q, seed=seed)
+        o = orc.autorank(A, b, l_max, eps, q=q, seed=seed)
+        tag = f"autorank {i}: m={m} n={n} b={b} l_max={l_max} eps={eps:.1e} q={q} {kind}"
+        assert g["l"] == o["l"], (tag, g["l"], o["l"])
+        l = g["l"]
+        Q = _np(g["Q"])
+        assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * max(l, 1), tag
+        rg = orc.residual(A, Q, _np(g["T"]), _np(g["P"])) / nA
+        ro = orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+        assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
+    else:
+        l = int(rng.integers(2, min(m, n, 160) + 1))
+        g = rq.tqlp(_cm(A), l)
+        o = orc.tqlp(A, l)
+        tag = f"tqlp {i}: m={m} n={n} l={l} {kind}"
+        Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+        assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
+        assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
+        rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+        assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
+        if kind != "numdef":
+            assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
+            Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
+            big = Lo >= 1e-4 * Lo.max()
+            assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
