@@ -504,6 +504,106 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       for (int r = threadIdx.x; r < rows; r += blockDim.x) a.M[(int64_t)(b + li * G) * a.ldm + r] = colbuf[(int64_t)li * rs + r];
 }
 
+// Small matrices (rows, cols <= 32, e.g. C1's 25 x 25 factor of the tail): the same factorisation
+// as hh_engine_kernel (pivot rule, xLARFG reflector, xLAQP2 downdating on squared norms, the
+// same outputs in M, Vst, tau, beta, perm, done) by ONE warp with lane c holding column c in
+// registers: the pivot column is broadcast by shuffles, and a step has no barrier at all
+// (the one-CTA engine spent ~4000 cycles per step on barriers and slot reductions).
+__global__ void __launch_bounds__(32, 1) hh_warp_kernel(EngineArgs a) {
+  const int lane = threadIdx.x, rows = a.rows, cols = a.cols;
+  const bool own = lane < cols;
+  double col[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) col[r] = (own && r < rows) ? a.M[(int64_t)lane * a.ldm + r] : 0.0;
+  double n1 = 0.0, r2 = 0.0;
+  bool done = !own;
+  if (own) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) n1 = fma(col[r], col[r], n1);
+    r2 = n1 != 0.0 ? 1.0 / n1 : 0.0;
+    a.done[lane] = 0;
+  }
+  for (int j = 0; j < a.steps; ++j) {
+    int p = j;
+    if (a.pivot) {
+      const Best c = warp_best(done ? Best{-1.0, 0x7fffffff} : Best{n1, lane});
+      p = c.i;
+    }
+    // the pivot column (all rows; rows < j are R entries and not used below)
+    double x[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x[r] = __shfl_sync(0xffffffffu, col[r], p);
+    // reflector, identically in every lane
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: the single warp is latency-bound
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r > j && r < rows) sq[r & 3] = fma(x[r], x[r], sq[r & 3]);
+    const double xn2 = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+    double alpha = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r == j) alpha = x[r];
+    double tau, beta, scal;
+    if (xn2 == 0.0) {
+      tau = 0.0; beta = alpha; scal = 0.0;
+    } else {
+      beta = -copysign(fast_sqrt(fma(alpha, alpha, xn2)), alpha);
+      const double amb = alpha - beta;
+      const double rinv = fast_rcp(beta * amb);
+      tau = -amb * amb * rinv;
+      scal = beta * rinv;
+    }
+    // outputs of the step: reflector column j (lane r writes row r), tau, beta, perm, done
+    {
+      double xr = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (lane == r) xr = x[r];
+      if (lane < rows) a.Vst[(int64_t)j * rows + lane] = lane < j ? 0.0 : (lane == j ? 1.0 : xr * scal);
+      if (lane == 0) { a.tau[j] = tau; a.beta[j] = beta; a.perm[j] = p; a.done[p] = 1; }
+    }
+    if (lane == p) done = true;
+    // apply H_j to every other live column, then downdate its norm
+    if (!done && tau != 0.0) {
+      double dd[4] = {0.0, 0.0, 0.0, 0.0}, xj = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r > j && r < rows) dd[r & 3] = fma(x[r], col[r], dd[r & 3]);
+        if (r == j) xj = col[r];
+      }
+      const double w = tau * fma(scal, (dd[0] + dd[1]) + (dd[2] + dd[3]), xj);
+      const double ws = w * scal;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r == j) col[r] = xj - w;
+        else if (r > j && r < rows) col[r] = fma(-ws, x[r], col[r]);
+      }
+    }
+    if (!done && a.pivot && n1 != 0.0) {
+      double xj = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r == j) xj = col[r];
+      double nn = fma(-xj, xj, n1);
+      nn = nn < 0.0 ? 0.0 : nn;
+      if (nn * r2 <= TOL3Z) {  // xLAQP2 recompute
+        double ss = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          if (r > j && r < rows) ss = fma(col[r], col[r], ss);
+        n1 = (j + 1 < rows) ? ss : 0.0;
+        r2 = n1 != 0.0 ? 1.0 / n1 : 0.0;
+      } else {
+        n1 = nn;
+      }
+    }
+  }
+  if (own)
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < rows) a.M[(int64_t)lane * a.ldm + r] = col[r];
+}
+
 // perm[steps..cols) = not-pivoted columns in ascending original order (single CTA scan).
 __global__ void compact_kernel(int cols, int steps, const int *done, int64_t *perm) {
   __shared__ int wsum[32];
@@ -639,7 +739,11 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
     const int64_t rs = round_up(rows, 2), op = round_up(owned, 2);
     return (size_t)(rs + 3 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;
   };
-  if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
+  if (rows <= 32 && cols <= 32) {
+    // one warp, columns in registers (no barriers): C1's 25 x 25 factor 52 -> ~6 us
+    hh_warp_kernel<<<1, 32, 0, c.stream>>>(a);
+    RQLP_LAUNCHED(c);
+  } else if (cols <= 256 && smem_for(cols, true) <= SMEM_MAX) {
     // whole matrix in one CTA's shared memory: no global exchange at all; the block is sized to
     // one 8-lane group per column (cheaper barriers for small matrices: C1's 25 x 25 factor
     // 64 -> 56 us).  Wider matrices go to the grid: an 8-lane group's column update is a
