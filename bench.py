@@ -290,8 +290,10 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    out = None
     for _ in range(args.warmup):
-        out = step()
+        out = None   # release the previous outputs first: the next call then gets the same buffers,
+        out = step()  # i.e. the same graph-cache key (eager, capture, then replays)
         flush_l2(flushbuf)
     barrier()
 
@@ -302,6 +304,7 @@ def main():
         barrier()
         for i in range(args.steps):
             flush_l2(flushbuf)
+            out = None
             ev[i][0].record(stream)
             out = step()
             ev[i][1].record(stream)
@@ -376,7 +379,7 @@ def main():
                 "apass_tflops": (passes(c) * flops_pass / (apass_total_ms * 1e-3) / 1e12) if apass_total_ms else None,
                 "tflops_effective": passes(c) * 2.0 * cg.m * c.n * c.l / (ms_per_step * 1e-3) / 1e12,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(),
+                "gpu_launches": launches, "clocks": clk.summary(), "step_ms": [round(t, 4) for t in step_ms],
                 "stages_ms": {k: round(sum(v) / len(v), 4) for k, v in stage_ms.items()},
                 "device_flags": flags}
         print(json.dumps(line), flush=True)
