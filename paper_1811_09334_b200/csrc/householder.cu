@@ -30,7 +30,12 @@ struct Best {
   double v;
   int i;
 };
-__device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
+// Candidate order: larger (squared) norm, then lower index.  A NaN norm (non-finite input) ranks
+// above every number, so a column is always chosen (the pivot index stays in range).
+__device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
+  if (v != v) return bv == bv || i < bi;
+  return v > bv || (v == bv && i < bi);
+}
 
 // Warp argmax (max value, lowest index on ties).  Values are >= 0 (squared norms) or -1 (no
 // candidate); non-negative doubles order like their bit patterns, so integer redux.sync on the

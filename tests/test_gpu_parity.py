@@ -471,3 +471,17 @@ def test_graph_replay_branches(rq, orc, make, flag, d):
     o = orc.rqlp(A, 12, 4, q=1, d=d, seed=7)
     ro = orc.residual(A, o["Q"], o["T"], o["P"])
     assert orc.residual(A, Q, T, P) <= 10 * ro + 1e-13 * max(np.linalg.norm(A), 1.0)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+@pytest.mark.parametrize("variant", [dict(q=1, d=0), dict(q=1, d=2), dict(q=0, b=4)])
+def test_nonfinite_input_terminates(rq, bad, variant):
+    """A non-finite entry in A must not hang any kernel (the Cholesky breakdown, the rescue's
+    grid barriers, the CPQR engine's exchange): the call returns and the output is non-finite
+    or flagged, never a deadlock."""
+    A = _rand_svd(300, 200, np.logspace(0, -3, 200), 3)
+    A[17, 23] = bad
+    h = rq.Handle()
+    g = rq.factorize(_cm(A), 10, 4, seed=1, handle=h, **variant)
+    h.sync()
+    assert g["Q"].shape == (300, 14)
