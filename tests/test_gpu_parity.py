@@ -485,3 +485,17 @@ def test_nonfinite_input_terminates(rq, bad, variant):
     g = rq.factorize(_cm(A), 10, 4, seed=1, handle=h, **variant)
     h.sync()
     assert g["Q"].shape == (300, 14)
+
+
+@pytest.mark.parametrize("scale", [1e200, 1e-200])
+def test_extreme_scale_terminates(rq, orc, scale):
+    """|A| near the double range limits: CholeskyQR's Grams and the CPQR's squared column norms
+    over/underflow (documented limit: max|A| sqrt(n) within ~1e+-150; scale A
+    first otherwise).  The call must still return without a fault or a hang."""
+    A = _rand_svd(300, 200, np.logspace(0, -3, 200), 4) * scale
+    h = rq.Handle()
+    g = rq.factorize(_cm(A), 10, 4, q=1, seed=1, handle=h)
+    flags = h.sync()
+    Q = _np(g["Q"])
+    ok = np.isfinite(Q).all() and np.abs(Q.T @ Q - np.eye(14)).max() <= 1e-12
+    print(f"scale {scale:g}: flags {flags}, Q finite and orthonormal: {ok}")
