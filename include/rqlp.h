@@ -46,7 +46,9 @@ extern "C" {
 
 /* rqlp_sync() flag bits */
 #define RQLP_FLAG_SHIFTED_CHOLQR 1u  /* a shifted CholeskyQR pass was needed (cond(Y) >~ 1e6) */
-#define RQLP_FLAG_RANK_DEFICIENT 2u  /* a basis column had to be completed (rank(Y) < l) */
+#define RQLP_FLAG_RANK_DEFICIENT 2u  /* a sketch was numerically rank deficient (a Cholesky pivot
+                                        <= 1e-15 of its Gram diagonal, i.e. a direction below
+                                        ~3e-8 relative) or a basis column was completed */
 
 typedef struct rqlp_handle_s *rqlp_handle_t;
 
