@@ -18,6 +18,7 @@ import torch
 from . import _capi
 
 __all__ = ["Handle", "RQLPError", "rqlp", "erqlp", "brqlp", "factorize", "factorize_host", "autorank", "tqlp",
+           "truncate",
            "omega", "gemm_nn", "gemm_tn", "orth", "cpqr", "qlp_tail", "residual", "rqlp_host", "cm_empty",
            "col_major", "lib", "VARIANT_RQLP", "VARIANT_ERQLP", "VARIANT_BRQLP"]
 
@@ -333,6 +334,24 @@ def residual(A, Q, T, P, handle=None) -> float:
     _check(lib().rqlp_residual_sq(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(T), _ld(T), _ptr(P), _ld(P),
                                   _ptr(out)), "rqlp_residual_sq")
     return float(out.item()) ** 0.5
+
+
+def truncate(out: dict, k: int, b: int | None = None) -> dict:
+    """Rank-k view of a factorisation (SPEC's truncation rule; no copy): A_k = Q[:, :k] T[:k, :k]
+    P[:, :k]^T with the first k pivots.  The factors are l-sized (the L-values are
+    |diag T|); truncation is a caller view.  For BRQLP (`b` given) k must fall on a block boundary,
+    since L = blkdiag(L_j) and P is orthonormal per block only (readings R14, R17)."""
+    l = out["T"].shape[0]
+    if not 1 <= k <= l:
+        raise ValueError(f"k = {k} outside 1..{l}")
+    if b is not None and k % b != 0 and k != l:
+        raise ValueError(f"BRQLP truncation must fall on a block boundary (b = {b})")
+    res = dict(out)
+    res["Q"], res["T"], res["P"] = out["Q"][:, :k], out["T"][:k, :k], out["P"][:, :k]
+    res["piv0"] = out["piv0"][:k]
+    if out.get("piv1") is not None:
+        res["piv1"] = out["piv1"][:k]
+    return res
 
 
 def factorize_host(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 0, b: int | None = None, seed: int = 0,

@@ -186,3 +186,23 @@ def test_random_sweep_autorank_tqlp(rq, orc, i):
             Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
             big = Lo >= 1e-4 * Lo.max()
             assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
+
+
+def test_truncate_views(rq, orc):
+    """Rank-k views: the truncated factors are views of the l-sized ones and the rank-k
+    approximation error is bounded by the l-sized residual plus the dropped L-values; BRQLP
+    truncation is refused off a block boundary."""
+    rng = np.random.default_rng(7)
+    sig = np.exp(-np.arange(1, 301.0) / 15)
+    A = _rand_A(rng, 500, 300, sig)
+    g = rq.factorize(_cm(A), 20, 8, q=1, d=2, seed=3)
+    t = rq.truncate(g, 20)
+    assert t["Q"].data_ptr() == g["Q"].data_ptr() and t["Q"].shape == (500, 20)
+    Q, T, P = _np(t["Q"]), _np(t["T"]), _np(t["P"])
+    nA = np.linalg.norm(A)
+    err = np.linalg.norm(A - Q @ T @ P.T) / nA
+    assert err <= 3 * sig[20] / sig[0] * np.sqrt(300) + orc.residual(A, _np(g["Q"]), _np(g["T"]), _np(g["P"])) / nA
+    gb = rq.factorize(_cm(A), 24, 8, q=1, b=8, seed=3)
+    assert rq.truncate(gb, 16, b=8)["T"].shape == (16, 16)
+    with pytest.raises(ValueError):
+        rq.truncate(gb, 20, b=8)
