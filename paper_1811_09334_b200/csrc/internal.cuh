@@ -62,6 +62,21 @@ __device__ __forceinline__ double fast_rcp(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
+// The completion vector of a dependent column (rank-deficient sketch, reading R4): a
+// SplitMix64-style hash of the counter (row + m column) -> two uniforms -> Box-Muller.  Any
+// N(0,1)-like fill works; orth.cu's replace_dep_kernel and orth_rescue.cu share it.
+__device__ __forceinline__ double completion_value(uint64_t ctr, uint64_t key) {
+  uint64_t z1 = ctr * 0x9E3779B97F4A7C15ULL + key;
+  z1 = (z1 ^ (z1 >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z1 = (z1 ^ (z1 >> 27)) * 0x94D049BB133111EBULL;
+  z1 ^= z1 >> 31;
+  uint64_t z2 = (ctr + 0x632BE59BD9B4E019ULL) * 0x9E3779B97F4A7C15ULL + key;
+  z2 = (z2 ^ (z2 >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z2 = (z2 ^ (z2 >> 27)) * 0x94D049BB133111EBULL;
+  z2 ^= z2 >> 31;
+  const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1p-53, u2 = (double)(z2 >> 11) * 0x1p-53;
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
 __device__ __forceinline__ double fast_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));

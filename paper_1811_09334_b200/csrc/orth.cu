@@ -321,28 +321,16 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   }
 }
 
-// dep[k] != 0: column k of Q (m x n) is replaced by a Philox N(0,1) vector (stream 7, counter =
-// row + m k); the next CholeskyQR pass orthonormalises it against the others (basis completion
+// dep[k] != 0: column k of Q (m x n) is replaced by a N(0,1)-like completion vector (counter =
+// row + m k, internal.cuh); the next CholeskyQR pass orthonormalises it against the others (basis completion
 // for rank-deficient input, reading R4/R21).
 __global__ void replace_dep_kernel(int64_t m, int n, double *Q, int64_t ldq, const int *dep, uint64_t seed,
                                    const unsigned *cond, unsigned cond_mask) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   for (int k = blockIdx.y; k < n; k += gridDim.y) {
     if (!dep[k]) continue;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-      uint64_t ctr = (uint64_t)(i + m * k), key = seed;
-      // SplitMix64-style hash -> two uniforms -> Box-Muller (any N(0,1)-like fill works here)
-      uint64_t z1 = ctr * 0x9E3779B97F4A7C15ULL + key;
-      z1 = (z1 ^ (z1 >> 30)) * 0xBF58476D1CE4E5B9ULL;
-      z1 = (z1 ^ (z1 >> 27)) * 0x94D049BB133111EBULL;
-      z1 ^= z1 >> 31;
-      uint64_t z2 = (ctr + 0x632BE59BD9B4E019ULL) * 0x9E3779B97F4A7C15ULL + key;
-      z2 = (z2 ^ (z2 >> 30)) * 0xBF58476D1CE4E5B9ULL;
-      z2 = (z2 ^ (z2 >> 27)) * 0x94D049BB133111EBULL;
-      z2 ^= z2 >> 31;
-      const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1p-53, u2 = (double)(z2 >> 11) * 0x1p-53;
-      Q[i + (int64_t)k * ldq] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
-    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+      Q[i + (int64_t)k * ldq] = completion_value((uint64_t)(i + m * k), seed);
   }
 }
 
