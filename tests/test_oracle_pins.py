@@ -332,6 +332,24 @@ def test_brqlp_deflated_power_step(orc):
     assert np.abs(r1["Q"].T @ r1["Q"] - np.eye(26)).max() < 1e-13 * 26
 
 
+@pytest.mark.parametrize("kind", ["rank_deficient", "gap"])
+def test_brqlp_reorth_twice_keeps_q_orthonormal(orc, kind):
+    """Reading R28: with Alg. 3 l.5 applied twice, Q stays orthonormal when a block lies (almost)
+    inside span(V_<j) -- beyond rank(A), or past a spectral gap -- where one pass cannot (in exact
+    arithmetic a block inside the span gives qr(0)); the residual is the exact-arithmetic one
+    (rank(A) <= l: ~0), a value fixed by the construction, not by the oracle."""
+    l = 30
+    sig = (np.r_[1.0 / np.arange(1, 16.0), np.zeros(185)] if kind == "rank_deficient"
+           else np.where(np.arange(1, 201) <= 20, 1.0, 1e-9) / np.arange(1, 201.0))
+    A = _rand_svd(400, 200, sig, 31)
+    out = orc.brqlp(A, 26, 4, b=4, q=0, seed=3)
+    Q = out["Q"]
+    assert np.abs(Q.T @ Q - np.eye(l)).max() < 1e-13 * l
+    res = orc.residual(A, Q, out["T"], out["P"]) / np.linalg.norm(A)
+    if kind == "rank_deficient":
+        assert res < 1e-13
+
+
 def test_corollary_expected_error_bound(orc):
     """Corollary (eq. (6), PAPER.md:112-119): E‖A−QLPᵀ‖_F ≤ (1+k/(p−1))^½ (Σ_{j>k} σ_j²)^½;
     sample mean over 20 seeds."""
