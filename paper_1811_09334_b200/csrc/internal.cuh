@@ -194,6 +194,7 @@ struct OrthScratch {
   size_t partial_elems = 0;
   double *scal = nullptr;       // small device scalars
   int *dep = nullptr;           // dependent-column flags of the last Cholesky (rank deficiency)
+  double *maxdev = nullptr;     // per-CTA max |G - I| of the second pass's near-identity test
 };
 void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms);
 // orth's rare branch (orth_rescue.cu): if (*cond & mask), repeated (shifted) CholeskyQR passes on

@@ -65,8 +65,22 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
                                                           unsigned *fail_word, unsigned fail_bit, int *dep,
                                                           unsigned dep_bit, unsigned *flag_word, const unsigned *cond,
                                                           unsigned cond_mask, int near_id, double shift_m,
-                                                          unsigned *shift_word, unsigned shift_bit) {
+                                                          unsigned *shift_word, unsigned shift_bit,
+                                                          const double *maxdev, int nmaxdev) {
   if (cond && ((*cond) & cond_mask) == 0) return;
+  if (near_id == 2) {
+    // near_id_spec_kernel already wrote the first-order factor; keep it if max|G - I| <= 2^-27
+    // (the per-CTA maxima are reduced here: no accumulator to reset between calls)
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nmaxdev; b += blockDim.x)
+      if (!(maxdev[b] <= 0x1p-27)) s_ok = 0;
+    __syncthreads();
+    if (s_ok) return;
+    if (threadIdx.x == 0) atomicOr(shift_word, shift_bit << 16);  // declined (as below)
+    near_id = 0;
+  }
   extern __shared__ double M[];  // npad x CB_LD, column-major: M[r + c * CB_LD]
   __shared__ double wkk[2][64];  // W_KK[i][t] at wkk[.][i * 8 + t] (unit lower), double-buffered
   __shared__ double dpiv[CHOL_SMALL], dinv[CHOL_SMALL], g0s[CHOL_SMALL], sq[CHOL_SMALL];
@@ -400,12 +414,56 @@ __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsign
 void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
                      const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0, int near_id = 0,
-                     double shift_m = 0.0, unsigned shift_bit = 0) {
+                     double shift_m = 0.0, unsigned shift_bit = 0, const double *maxdev = nullptr,
+                     int nmaxdev = 0) {
   smem_attr((const void *)chol_blk_kernel, CHOL_SMALL * CB_LD * 8);
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
-      near_id, shift_m, c.dflags + COND_WORD, shift_bit);
+      near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev);
   RQLP_LAUNCHED(c);
+}
+
+// CholeskyQR2's second pass, speculatively and grid-wide: every entry of the upper triangle gets
+// the first-order factor R = I + U, X = I - U (U = triu(E, 1) + diag(E)/2, E = G - I; the
+// strictly lower parts zero), and max |E| over the upper triangle goes to *maxbits (ordered
+// bits; NaN ranks highest).  chol_blk_kernel (near_id = 2) keeps this when max |E| <= 2^-27 and
+// otherwise factorises and overwrites R and X.  (In one CTA the same test sat behind a ~4 us
+// latency-bound load of G.)
+__global__ void near_id_spec_kernel(int n, const double *__restrict__ G, int64_t ldg, double *__restrict__ R,
+                                    int64_t ldr, double *__restrict__ X, int64_t ldx, double *maxdev,
+                                    const unsigned *cond, unsigned cond_mask) {
+  __shared__ double wmax[8];
+  if (cond && ((*cond) & cond_mask) == 0) return;
+  const int64_t total = (int64_t)n * n;
+  double e = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q % n), j = (int)(q / n);
+    double r = 0.0, x = 0.0;
+    if (i <= j) {
+      const double dlt = i == j ? 1.0 : 0.0;
+      const double E = G[i + (int64_t)j * ldg] - dlt;
+      const double aE = fabs(E);
+      if (!(aE <= e)) e = aE;  // NaN propagates
+      const double u = i < j ? E : 0.5 * E;
+      r = dlt + u;
+      x = dlt - u;
+    }
+    R[i + (int64_t)j * ldr] = r;
+    X[i + (int64_t)j * ldx] = x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, e, o);
+    if (!(t <= e)) e = t;
+  }
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bm = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      if (!(wmax[w] <= bm)) bm = wmax[w];
+    maxdev[blockIdx.x] = bm;  // this CTA's max |E|
+  }
 }
 
 }  // namespace
@@ -465,6 +523,7 @@ void orth_carve(Arena &a, OrthScratch &s, int64_t m, int64_t c, int num_sms) {
   s.partials = a.take<double>((int64_t)s.partial_elems);
   s.scal = a.take<double>(8);
   s.dep = a.take<int>(c);
+  s.maxdev = a.take<double>(256);
 }
 
 // One CholeskyQR pass: Qout = Yin R^-1 with G = Yin^T Yin.  pass_bit marks this pass's
@@ -483,8 +542,18 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
   if (n <= CHOL_SMALL) {
     // one kernel: near-identity factor (second pass), else Cholesky + inverse, and on breakdown
     // the shifted retry in place (marks pass_bit << 8 for the third pass)
+    // second pass: the near-identity test and first-order factor grid-wide ahead of the Cholesky
+    // kernel when n >= 64 (for smaller n the in-kernel test is cheaper than another launch)
+    const bool spec = second && n >= 64;
+    int nblk = 0;
+    if (spec) {
+      nblk = (int)std::min<int64_t>(ceil_div(n * n, 256), std::min<int64_t>(c.num_sms, 256));
+      near_id_spec_kernel<<<nblk, 256, 0, c.stream>>>((int)n, s.G, lc, Rout, lc, s.Rinv, lc, s.maxdev, cond, mask);
+      RQLP_LAUNCHED(c);
+    }
     launch_chol_inv(c, (int)n, s.G, lc, s.G, lc, Rout, lc, s.Rinv, lc, condw, 0u, cond, mask,
-                    use_dep ? s.dep : nullptr, dep_bit, second ? 1 : 0, (double)m, pass_bit << 8);
+                    use_dep ? s.dep : nullptr, dep_bit, spec ? 2 : (second ? 1 : 0), (double)m, pass_bit << 8,
+                    s.maxdev, nblk);
   } else {
     if (second) {
       // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
