@@ -611,29 +611,41 @@ __global__ void __launch_bounds__(32, 1) hh_warp_kernel(EngineArgs a) {
 
 // perm[steps..cols) = not-pivoted columns in ascending original order (single CTA scan).
 __global__ void compact_kernel(int cols, int steps, const int *done, int64_t *perm) {
+  // each thread owns a run of CPT consecutive columns: all flags are loaded before the scan (one
+  // memory round trip instead of one per 1024-column chunk), then a single block scan of the
+  // per-thread counts places every run
+  constexpr int CPT = 16;
   __shared__ int wsum[32];
-  __shared__ int base;
-  if (threadIdx.x == 0) base = steps;
-  __syncthreads();
-  for (int c0 = 0; c0 < cols; c0 += blockDim.x) {
-    int i = c0 + threadIdx.x;
-    int flag = (i < cols && !done[i]) ? 1 : 0;
-    // block exclusive scan
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned bal = __ballot_sync(0xffffffffu, flag);
-    int pre = __popc(bal & ((1u << lane) - 1));
-    if (lane == 0) wsum[warp] = __popc(bal);
-    __syncthreads();
-    int off = 0;
-    for (int w = 0; w < warp; ++w) off += wsum[w];
-    if (flag) perm[base + off + pre] = i;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
-      base += tot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c0 = 0; c0 < cols; c0 += CPT * (int)blockDim.x) {
+    const int first = c0 + threadIdx.x * CPT;
+    int fl[CPT];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      fl[u] = (first + u < cols) ? !done[first + u] : 0;
+      cnt += fl[u];
     }
+    // exclusive scan of cnt over the block (warp shuffles, then warp totals)
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
     __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < warp) off += wsum[w];
+      tot += wsum[w];
+    }
+    int pos = steps + off + inc - cnt;
+#pragma unroll
+    for (int u = 0; u < CPT; ++u)
+      if (fl[u]) perm[pos++] = first + u;
+    __syncthreads();
+    steps += tot;  // the next chunk's base (every thread computed the same total)
   }
 }
 
