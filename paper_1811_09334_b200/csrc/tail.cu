@@ -21,33 +21,31 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
 
 namespace {
 
+// D(:, t) = S(:, perm[t]); also copies perm[0..cols) to piv_out when given (one launch less)
 __global__ void gather_cols_kernel(int64_t rows, int64_t cols, const double *S, int64_t lds, const int64_t *perm,
-                                   double *D, int64_t ldd) {
+                                   double *D, int64_t ldd, int64_t *piv_out = nullptr) {
   int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e % rows, t = e / rows;
     D[i + t * ldd] = S[i + perm[t] * lds];
+    if (piv_out && i == 0) piv_out[t] = perm[t];
   }
 }
 
-// D(perm[i], :) = S(i, :)
+// D(perm[i], :) = S(i, :); also copies perm[0..npiv) to piv_out when given (one launch less)
 __global__ void scatter_rows_kernel(int64_t rows, int64_t cols, const double *S, int64_t lds, const int64_t *perm,
-                                    double *D, int64_t ldd) {
+                                    double *D, int64_t ldd, int64_t *piv_out = nullptr, int64_t npiv = 0) {
   int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e % rows, j = e / rows;
     D[perm[i] + j * ldd] = S[i + j * lds];
+    if (piv_out && j == 0 && i < npiv) piv_out[i] = perm[i];
   }
 }
 
 __global__ void iota_kernel(int64_t count, int64_t *dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = i;
-}
-
-__global__ void copy_i64_kernel(int64_t count, const int64_t *src, int64_t *dst) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = src[i];
 }
 
 int grid_for(Ctx &c, int64_t total) {
@@ -84,18 +82,15 @@ static double *pivoted_lq(Ctx &c, TailScratch &s, int64_t rows, int64_t l, int64
                           double *T, int64_t ldt, double *QB, int64_t ldqb, int64_t *piv1) {
   const int64_t ldn = s.ldn, ldl = s.ldl;
   launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, false);
-  hh_factor(c, s.hh, l, l, s.Mt, ldl, true);
-  copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.hh.perm, s.perm1);
-  RQLP_LAUNCHED(c);
-  hh_extract_r(c, s.hh, l, l, s.Mt, ldl, T, ldt, true);  // L = (L^T)^T, lower
-  hh_form_q(c, s.hh, l, l, s.Qt, ldl);
+  HHScratch h1 = s.hh;
+  h1.perm = s.perm1;  // the engine's permutation lands in perm1 directly (no copy)
+  hh_factor(c, h1, l, l, s.Mt, ldl, true);
+  hh_extract_r(c, h1, l, l, s.Mt, ldl, T, ldt, true);  // L = (L^T)^T, lower
+  hh_form_q(c, h1, l, l, s.Qt, ldl);
   gemm_nn(c, n, l, l, s.Qhat, ldn, s.Qt, ldl, s.tmp_nl, ldn, s.orth.partials, s.orth.partial_elems);  // Q1
-  gather_cols_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(rows, l, Q0, ldq0, s.perm1, QB, ldqb);  // Q0 Π1
+  gather_cols_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(rows, l, Q0, ldq0, s.perm1, QB, ldqb,
+                                                                   piv1);  // Q0 Π1 (and piv1)
   RQLP_LAUNCHED(c);
-  if (piv1) {
-    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm1, piv1);
-    RQLP_LAUNCHED(c);
-  }
   return s.tmp_nl;
 }
 
@@ -103,14 +98,14 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
               double *T, int64_t ldt, double *PB, int64_t ldpb, int64_t *piv0, int64_t *piv1) {
   const int64_t ldn = s.ldn, ldl = s.ldl;
   // [Q0, R0, Π0] = cpqr(B)  (Alg.1 l.5)
-  hh_factor(c, s.hh, l, n, B, ldb, true);
-  copy_i64_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, s.hh.perm, s.perm0);
-  RQLP_LAUNCHED(c);
-  hh_extract_r(c, s.hh, l, n, B, ldb, s.Rt, ldn, true);   // R0^T, n x l
+  HHScratch h0 = s.hh;
+  h0.perm = s.perm0;  // the engine's permutation lands in perm0 directly (no copy)
+  hh_factor(c, h0, l, n, B, ldb, true);
+  hh_extract_r(c, h0, l, n, B, ldb, s.Rt, ldn, true);   // R0^T, n x l
   // Q0 (l x l) is needed only at the assembly: formed on the side stream while the main stream
   // orthonormalises R0^T (the join precedes the next use of the reflector store s.hh)
   Ctx side = c.branch();
-  hh_form_q(side, s.hh, l, n, s.Q0, ldl);
+  hh_form_q(side, h0, l, n, s.Q0, ldl);
   c.mark("tail_cpqr_B");
   // R0^T = Q^ R^ (CholeskyQR2; the tall part of cpqr(R0^T) / the i = 1 inner QR)
   orth(c, s.orth, n, l, s.Rt, ldn, s.Qhat, ldn, s.Rhat, ldl);
@@ -144,13 +139,9 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
       RQLP_LAUNCHED(c);
     }
   }
-  // P_B = Π0 P1: row perm0[i] of P_B is row i of P1
-  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, PB, ldpb);
+  // P_B = Π0 P1: row perm0[i] of P_B is row i of P1 (and piv0 = perm0[0..l))
+  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, PB, ldpb, piv0, l);
   RQLP_LAUNCHED(c);
-  if (piv0) {
-    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm0, piv0);
-    RQLP_LAUNCHED(c);
-  }
   c.mark("tail_assemble");
 }
 
@@ -162,20 +153,16 @@ void tqlp(Ctx &c, TailScratch &s, HHScratch &hA, int64_t m, int64_t n, int64_t l
           int64_t ldq, double *L, int64_t ldl_out, double *P, int64_t ldp, int64_t *piv0, int64_t *piv1, double *QR,
           int64_t ldqr) {
   const int64_t ldn = s.ldn, ldl = s.ldl;
-  hh_factor(c, hA, m, n, W, ldw, true, l);                  // partial CPQR, l steps
-  copy_i64_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, hA.perm, s.perm0);
-  RQLP_LAUNCHED(c);
-  hh_extract_r(c, hA, m, n, W, ldw, s.Rt, ldn, true, l);     // [R11 R12]^T, n x l
-  hh_form_q(c, hA, m, n, QR, ldqr, l);                      // Q_R, m x l
+  HHScratch ha = hA;
+  ha.perm = s.perm0;  // the engine's permutation lands in perm0 directly (no copy)
+  hh_factor(c, ha, m, n, W, ldw, true, l);                  // partial CPQR, l steps
+  hh_extract_r(c, ha, m, n, W, ldw, s.Rt, ldn, true, l);     // [R11 R12]^T, n x l
+  hh_form_q(c, ha, m, n, QR, ldqr, l);                      // Q_R, m x l
   c.mark("tqlp_cpqr_A");
   orth(c, s.orth, n, l, s.Rt, ldn, s.Qhat, ldn, s.Rhat, ldl);
   double *PO = pivoted_lq(c, s, m, l, n, QR, ldqr, L, ldl_out, Q, ldq, piv1);
-  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, P, ldp);
+  scatter_rows_kernel<<<grid_for(c, n * l), 256, 0, c.stream>>>(n, l, PO, ldn, s.perm0, P, ldp, piv0, l);
   RQLP_LAUNCHED(c);
-  if (piv0) {
-    copy_i64_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, s.perm0, piv0);
-    RQLP_LAUNCHED(c);
-  }
   c.mark("tqlp_tail");
 }
 
