@@ -118,22 +118,30 @@ void qlp_tail(Ctx &c, TailScratch &s, int64_t l, int64_t n, double *B, int64_t l
     PO = s.Qhat;
     double *Pspare = s.tmp_nl;
     double *qe = s.Q0, *qe_spare = s.QE;  // Q^(0) Q^(2) ..., ping-pong (no copies)
+    int64_t ldqe = ldl;
+    const int last_even = d % 2 == 0 ? d : d - 1;
     for (int i = 2; i <= d; ++i) {
       // [Q^(i), R^(i)] = qr([R^(i-1)]^T): unpivoted, so CholeskyQR2 gives the same unique
       // factors (R_ii > 0) as Householder to rounding (reading R3).  R^(i) overwrites R^(i-1)
-      // in Rhat (the input is the transposed copy in Mt).
+      // in Rhat (the input is the transposed copy in Mt); for even d the last R^(d) is T itself.
       launch_copy(c, l, l, s.Rhat, ldl, s.Mt, ldl, true);   // [R^(i-1)]^T
-      orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, s.Rhat, ldl, false);
+      const bool r_to_t = i == d && d % 2 == 0;
+      orth(c, s.orth, l, l, s.Mt, ldl, s.Qt, ldl, r_to_t ? T : s.Rhat, r_to_t ? ldt : ldl, false);
       if (i % 2 == 0) {
-        gemm_nn(c, l, l, l, qe, ldl, s.Qt, ldl, qe_spare, ldl, s.orth.partials, s.orth.partial_elems);
-        std::swap(qe, qe_spare);
+        // the last even product goes straight to QB
+        double *dst = i == last_even ? QB : qe_spare;
+        const int64_t ldd = i == last_even ? ldqb : ldl;
+        gemm_nn(c, l, l, l, qe, ldqe, s.Qt, ldl, dst, ldd, s.orth.partials, s.orth.partial_elems);
+        qe_spare = qe;
+        qe = dst;
+        ldqe = ldd;
       } else {
         gemm_nn(c, n, l, l, PO, ldn, s.Qt, ldl, Pspare, ldn, s.orth.partials, s.orth.partial_elems);
         std::swap(PO, Pspare);
       }
     }
-    launch_copy(c, l, l, s.Rhat, ldl, T, ldt, d % 2 == 1);   // T = [R^(d)]^T (odd d) or R^(d) (even d)
-    launch_copy(c, l, l, qe, ldl, QB, ldqb, false);
+    if (d % 2 == 1) launch_copy(c, l, l, s.Rhat, ldl, T, ldt, true);   // T = [R^(d)]^T (odd d)
+    if (last_even < 2) launch_copy(c, l, l, qe, ldl, QB, ldqb, false);  // d = 1: Q_B = Q^(0)
     if (piv1) {
       iota_kernel<<<grid_for(c, l), 256, 0, c.stream>>>(l, piv1);
       RQLP_LAUNCHED(c);
