@@ -66,8 +66,11 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
                                                           unsigned dep_bit, unsigned *flag_word, const unsigned *cond,
                                                           unsigned cond_mask, int near_id, double shift_m,
                                                           unsigned *shift_word, unsigned shift_bit,
-                                                          const double *maxdev, int nmaxdev) {
+                                                          const double *maxdev, int nmaxdev, int zero_cond) {
   if (cond && ((*cond) & cond_mask) == 0) return;
+  // the first pass of an orth clears the COND word itself (instead of a memset node): no other
+  // kernel of the orth has touched it yet, and the bits below are set after barriers
+  if (zero_cond && threadIdx.x == 0) *shift_word = 0u;
   if (near_id == 2) {
     // near_id_spec_kernel already wrote the first-order factor; keep it if max|G - I| <= 2^-27
     // (the per-CTA maxima are reduced here: no accumulator to reset between calls)
@@ -415,11 +418,11 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
                      const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0, int near_id = 0,
                      double shift_m = 0.0, unsigned shift_bit = 0, const double *maxdev = nullptr,
-                     int nmaxdev = 0) {
+                     int nmaxdev = 0, int zero_cond = 0) {
   smem_attr((const void *)chol_blk_kernel, CHOL_SMALL * CB_LD * 8);
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
-      near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev);
+      near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev, zero_cond);
   RQLP_LAUNCHED(c);
 }
 
@@ -553,7 +556,7 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
     }
     launch_chol_inv(c, (int)n, s.G, lc, s.G, lc, Rout, lc, s.Rinv, lc, condw, 0u, cond, mask,
                     use_dep ? s.dep : nullptr, dep_bit, spec ? 2 : (second ? 1 : 0), (double)m, pass_bit << 8,
-                    s.maxdev, nblk);
+                    s.maxdev, nblk, (pass_bit == 1u && !cond && !sharded) ? 1 : 0);
   } else {
     if (second) {
       // near-identity Gram: elementwise factor; the full Cholesky below runs only if it declines
@@ -623,7 +626,8 @@ void orth(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const double *Y, int64_t
           double *R, int64_t ldr, bool sharded, bool span_only) {
   int64_t lc = round_up(n, 8);
   unsigned *condw = c.dflags + COND_WORD;
-  RQLP_CUDA(cudaMemsetAsync(condw, 0, sizeof(unsigned), c.stream));
+  // the fused first pass (n <= 128, one device) clears the COND word in its Cholesky kernel
+  if (sharded || n > CHOL_SMALL) RQLP_CUDA(cudaMemsetAsync(condw, 0, sizeof(unsigned), c.stream));
   if (span_only && !R) {
     // intermediate subspace-iteration basis: only range(V) = range(Y) matters (V = Y R^-1 for any
     // invertible R keeps the span to the same O(u cond(Y)) rounding), so one CholeskyQR pass.
