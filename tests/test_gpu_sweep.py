@@ -206,3 +206,38 @@ def test_truncate_views(rq, orc):
     assert rq.truncate(gb, 16, b=8)["T"].shape == (16, 16)
     with pytest.raises(ValueError):
         rq.truncate(gb, 20, b=8)
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_sweep_large_blocks(rq, orc, i):
+    """Larger BRQLP and auto-rank cases: many blocks (ragged last), q up to 2, l up to ~300 (the
+    blocked Cholesky past 128 columns inside the block orths' reorthogonalisation)."""
+    rng = np.random.default_rng(12000 + i)
+    k = int(rng.integers(40, 260))
+    p = int(rng.integers(2, 24))
+    l = k + p
+    m = int(rng.integers(max(l, 1200), 3600))
+    n = int(rng.integers(max(l, 900), 2800))
+    q = int(rng.integers(0, 3))
+    b = int(rng.integers(8, min(150, l) + 1))   # 1 <= b <= l
+    kind, sig = _spectrum(rng, min(m, n, 3 * l), k, l)
+    A = _rand_A(rng, m, n, sig)
+    seed = int(rng.integers(0, 2**62))
+    nA = np.linalg.norm(A)
+    tag = f"large-blocks {i}: m={m} n={n} k={k} p={p} q={q} b={b} {kind}"
+    if i % 3 == 2:
+        eps = float(10 ** rng.uniform(-5, -1))
+        g = rq.autorank(_cm(A), b=b, l_max=l, eps=eps, q=q, seed=seed)
+        o = orc.autorank(A, b, l, eps, q=q, seed=seed)
+        assert g["l"] == o["l"], (tag, g["l"], o["l"])
+        lq = g["l"]
+    else:
+        g = rq.factorize(_cm(A), k, p, q=q, b=b, seed=seed)
+        o = orc.brqlp(A, k, p, b=b, q=q, seed=seed)
+        lq = l
+    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+    assert np.abs(Q.T @ Q - np.eye(lq)).max() <= 1e-13 * lq, tag
+    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+    assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
+    if kind != "numdef":
+        assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
