@@ -241,3 +241,31 @@ def test_random_sweep_large_blocks(rq, orc, i):
     assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
     if kind != "numdef":
         assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
+
+
+_EDGE = [(l, sh, q, d) for l in (4, 32, 33, 128, 129, 257) for sh in ("square", "tall", "wide", "l_plus_1")
+         for (q, d) in ((0, 0), (2, 3))]
+
+
+@pytest.mark.parametrize("l,shape,q,d", _EDGE)
+def test_edge_shapes(rq, orc, l, shape, q, d):
+    """Shapes at the path switches: m or n equal to l (square sketch / B), l at the one-warp CPQR
+    limit (32/33), at the fused Cholesky limit (128/129), past the one-CTA engine (257)."""
+    m, n = {"square": (l, l), "tall": (3 * l, l), "wide": (l, 3 * l), "l_plus_1": (l + 1, l + 1)}[shape]
+    rng = np.random.default_rng(l * 7 + len(shape) + q + d)
+    sig = np.exp(-np.arange(1, min(m, n) + 1.0) / max(4.0, l / 4))
+    A = _rand_A(rng, m, n, sig)
+    k, p = l - 2, 2
+    g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=5)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=5)
+    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
+    nA = np.linalg.norm(A)
+    tag = f"edge l={l} {shape} q={q} d={d}"
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
+    assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
+    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
+    assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
+    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
+    Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
+    big = Lo >= 1e-4 * Lo.max()
+    assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
