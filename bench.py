@@ -3,13 +3,17 @@
 
 One "step" = one whole factorisation (Ω, every A-pass, orthonormalisations, the CPQR/QLP
 tail and the assembly of Q, T, P) of the workload's synthetic matrix, already resident in
-HBM.  Default workload: BASELINE.json configs[1] ("c2": ERQLP fp64, m = n = 4096, k = 100,
-p = 10, q = 1, d = 2).  Prints ONE JSON line (rank 0).
+HBM.  Default workload: BASELINE.json configs[3] ("c4": Block RQLP fp64, m = 262144,
+n = 16384, k = 512, p = 16, b = 64, q = 1) -- the configuration the metric is quoted on at
+1/2/4/8 B200 and the largest one that fits one GPU.  Prints ONE JSON line (rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c1e|c2|c3|c4|c5w]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c1e|c2|c3|c4|c5|c5w]
+                  [--scaling strong|weak]
   python bench.py --impl reference ...   # the CPU oracle (oracle/) timed on this host's cores
-For N > 1 launch with torchrun (one rank per GPU, NCCL); A is row-sharded with the per-rank
-row count of the workload fixed (weak scaling: global m = N x m_workload).
+For N > 1 launch with torchrun (one rank per GPU, NCCL).  A is row-sharded.  --scaling strong
+(default for c4 and c5, BASELINE's 1/2/4/8-GPU configs) keeps the global m of the workload and
+gives each rank ~m/N rows; --scaling weak (default for c5w) keeps m rows per rank (global m =
+N x m).
 """
 from __future__ import annotations
 
@@ -31,7 +35,7 @@ from synthetic import CONFIGS, make_A_config  # noqa: E402
 
 FP64_DMMA_PEAK_TFLOPS = 37.07   # measured: tools/microbench/fp64_peak.cu on this pool (profiles/r01_fp64_peak.txt)
 FP64_NOMINAL_TFLOPS = 37.2      # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
-METRIC = "RQLP sec/factorization"
+METRIC = "RQLP sec/factorization; A-pass TFLOP/s as % roofline at 1/2/4/8 B200"
 
 
 def log(*a):
@@ -179,78 +183,149 @@ def load_traffic(name: str):
 
 
 # ---------------------------------------------------------------------------- oracle arm
-def oracle_time(A_np, c, budget_s: float = 12.0):
-    """Time the CPU oracle (as it stands) on a bounded sample of workload c.  Returns
-    (sec_per_factorisation_estimate, sample description, threads)."""
+def _oracle_run(A_np, c):
+    import oracle
+    if c.b is not None:
+        oracle.brqlp(A_np, c.k, c.p, b=c.b, q=c.q, seed=c.seed)
+    else:
+        oracle.rqlp(A_np, c.k, c.p, q=c.q, d=c.d, seed=c.seed)
+
+
+def sample_rows(c, budget_s: float, threads: int) -> int:
+    """Rows of the bounded oracle sample: the A-passes scale with m (the tail does not), so the
+    first m_s rows with the same n, k, p, q, d, b cost ~ m_s/m of the whole factorisation."""
+    full_work = passes(c) * 2.0 * c.m * c.n * c.l
+    gflops_guess = 15.0 * threads / 8
+    m_s = c.m
+    if full_work / (gflops_guess * 1e9) > budget_s:
+        m_s = max(c.l + 1, int(c.m * budget_s * gflops_guess * 1e9 / full_work))
+    return min(c.m, m_s)
+
+
+def oracle_time(A_rows, c, budget_s: float = 12.0, reps_max: int = 5):
+    """Time the CPU oracle (as it stands) on a bounded sample of workload c.  `A_rows(m_s)` returns
+    the first m_s rows of A as a column-major numpy array.  Returns (sec_per_factorisation_estimate,
+    sample description, threads)."""
     import oracle
     oracle.build()
-    m = A_np.shape[0]
-    full_work = passes(c) * 2.0 * c.m * c.n * c.l
-    # sample: the first m_s rows of A (same n, k, p, q, d, b) -- the A-passes scale with m, the
-    # tail does not, so sec(full) ~= sec(sample) * m / m_s is an upper-bound-leaning estimate.
-    gflops_guess = 15.0 * oracle.num_threads() / 8
-    m_s = m
-    if full_work / (gflops_guess * 1e9) > budget_s:
-        m_s = max(c.l + 1, int(m * budget_s * gflops_guess * 1e9 / full_work))
-        m_s = min(m, m_s)
-    As = A_np[:m_s]
+    th = oracle.num_threads()
+    m_s = sample_rows(c, budget_s, th)
+    As = A_rows(m_s)
     reps, t_tot = 0, 0.0
     while True:
         t0 = time.perf_counter()
-        if c.b is not None:
-            oracle.brqlp(As, c.k, c.p, b=c.b, q=c.q, seed=c.seed)
-        else:
-            oracle.rqlp(As, c.k, c.p, q=c.q, d=c.d, seed=c.seed)
+        _oracle_run(As, c)
         t_tot += time.perf_counter() - t0
         reps += 1
-        if t_tot >= budget_s * 0.5 or reps >= 5:
+        if t_tot >= budget_s * 0.5 or reps >= reps_max:
             break
-    sec = t_tot / reps * (m / m_s)
-    sample = (f"{reps} oracle factorisation(s) of the first {m_s} of {m} rows (n={c.n}, l={c.l}, q={c.q}, d={c.d}"
-              + (f", b={c.b}" if c.b else "") + ")" + (f", scaled by m/m_s={m / m_s:.2f}" if m_s < m else ""))
-    return sec, sample, oracle.num_threads()
+    sec = t_tot / reps * (c.m / m_s)
+    sample = (f"{reps} oracle factorisation(s) of the first {m_s} of {c.m} rows (n={c.n}, l={c.l}, q={c.q}, d={c.d}"
+              + (f", b={c.b}" if c.b else "") + ")" + (f", scaled by m/m_s={c.m / m_s:.2f}" if m_s < c.m else ""))
+    return sec, sample, th
 
 
-def run_reference(args, c):
+def single_thread_times() -> dict:
+    """The oracle on ONE host thread at C1 (whole factorisation) and C2 (whole factorisation,
+    one run): SURVEY §8(d)'s single-thread CPU figures."""
+    import oracle
+    from synthetic import CONFIGS as C
+    out = {}
+    prev = oracle.num_threads()
+    oracle.set_num_threads(1)
+    try:
+        for name in ("c1", "c2"):
+            c = C[name]
+            A = make_A_config(c, device="cuda" if torch.cuda.is_available() else "cpu").cpu().numpy()
+            t0 = time.perf_counter()
+            _oracle_run(A, c)
+            out[name] = round(time.perf_counter() - t0, 4)
+    finally:
+        oracle.set_num_threads(prev)
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def config_dict(c, world: int, scaling: str, m_global: int) -> dict:
+    """The `config` object of the JSON line -- identical for both arms."""
+    return {**describe(c), "global_m": m_global, "scaling": scaling,
+            "parallelism": f"rows of A sharded over {world} rank(s) ({scaling} scaling)",
+            "l2": "flushed between timed steps (256 MB write, untimed); A alone is larger than L2"}
+
+
+def resolve(args):
+    c = CONFIGS[args.workload]
+    scaling = args.scaling or ("weak" if c.name == "c5w" else "strong")
+    return c, scaling
+
+
+def run_reference(args, c, scaling):
+    """--impl reference: the CPU oracle as it stands on the host cores, on a bounded row sample of
+    the workload (rank 0 only; other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    torch.manual_seed(0)
-    A = make_A_config(c, device="cpu")
-    A_np = A.numpy()  # column-major view (m, n)
+    import dataclasses
     import oracle
     oracle.build()
+    cg = dataclasses.replace(c, m=c.m * world) if scaling == "weak" else c
+    th = oracle.num_threads()
+    m_s = sample_rows(cg, 5.0, th)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"   # data generation only (torch), not the method
+    A_s = make_A_config(cg, device=dev, row_range=(0, m_s)).cpu().numpy()
+    if dev == "cuda":
+        torch.cuda.empty_cache()
     secs = []
+    sample = ""
     for i in range(args.warmup + args.steps):
-        s, sample, th = oracle_time(A_np, c, budget_s=6.0)
+        s, sample, th = oracle_time(lambda ms: A_s[:ms], cg, budget_s=5.0, reps_max=1)
         if i >= args.warmup:
             secs.append(s)
     val = sum(secs) / len(secs)
     line = {"metric": METRIC, "value": val, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": describe(c),
-            "cpu_baseline": {"value": val, "unit": "s", "cores": th, "kind": "oracle", "sample": sample},
+            "config": config_dict(c, world, scaling, cg.m),
+            "cpu_baseline": {"value": val, "unit": "s", "cores": th, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------- GPU arm
+DEFAULT_STEPS = {"c1": (20, 5), "c1e": (20, 5), "c2": (20, 5), "c3": (10, 3), "c4": (5, 3), "c5": (3, 3),
+                 "c5w": (3, 3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--workload", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    c = CONFIGS[args.workload]
+    ds, dw = DEFAULT_STEPS.get(args.workload, (5, 3))
+    args.steps = ds if args.steps is None else args.steps
+    args.warmup = max(dw if args.warmup is None else args.warmup, 3)
+    c, scaling = resolve(args)
     if args.impl == "reference":
-        return run_reference(args, c)
+        return run_reference(args, c, scaling)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,16 +342,17 @@ def main():
     from paper_1811_09334_b200 import build as rqbuild
     rqbuild.build()
 
-    # A: per-rank row block of the weak-scaled matrix (global m = world * c.m)
     import dataclasses
 
     from paper_1811_09334_b200.dist import max_over_ranks, row_block
-    cg = dataclasses.replace(c, m=c.m * world)
+    cg = dataclasses.replace(c, m=c.m * world) if scaling == "weak" else c
     r0, r1 = row_block(cg.m, rank, world)
+    m_loc = r1 - r0
     t0 = time.time()
     A = make_A_config(cg, device=dev, row_range=(r0, r1) if world > 1 else None)
     torch.cuda.synchronize()
-    log(f"[bench] rank {rank}: A {tuple(A.shape)} generated in {time.time() - t0:.1f}s")
+    torch.cuda.empty_cache()
+    log(f"[bench] rank {rank}: A {tuple(A.shape)} (rows {r0}..{r1} of {cg.m}) generated in {time.time() - t0:.1f}s")
     handle = rq.Handle(device=dev, group=group)
     handle.set_timing(True)
     flushbuf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
@@ -296,6 +372,14 @@ def main():
         out = step()  # i.e. the same graph-cache key (eager, capture, then replays)
         flush_l2(flushbuf)
     barrier()
+    if world > 1:   # the replicated outputs (L, P, pivots) must be bit-identical on every rank
+        chk = torch.stack([out["T"].contiguous().view(torch.int64).sum(), out["P"].contiguous().view(torch.int64).sum(),
+                           out["piv0"].sum()])
+        allc = [torch.zeros_like(chk) for _ in range(world)]
+        torch.distributed.all_gather(allc, chk)
+        replicated_identical = all(torch.equal(allc[0], x) for x in allc)
+    else:
+        replicated_identical = True
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stage_ms: dict[str, list[float]] = {}
@@ -315,77 +399,91 @@ def main():
     # in the e2e number).  The stage events are those of the last timed step.
     for name, ms in handle.timing():
         stage_ms.setdefault(name, []).append(ms)
-    stage_steps = 1
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), group, dev)
     ms_per_step = total_ms / args.steps
     flags = handle.sync()
 
-    # ---- A-pass roofline (the hot path: 92-97% of the flops): algorithmic A-pass flops per step
-    # (passes x 2 m n l; BRQLP: the width-l sketch + (2q+1) width-b_j passes per block, same
-    # total) / the summed per-pass CUDA-event durations inside the timed region.
+    # ---- A-pass roofline (the dominant kernel: 92-97% of the flops).  Algorithmic A-pass flops per
+    # width-l-equivalent pass on this rank (2 m_loc n l; BRQLP: the width-l sketch + (2q+1)
+    # width-b_j passes per block, the same total) / the mean per-pass CUDA-event duration inside the
+    # timed region (stage events of the last timed step, on the library's stream); max over ranks.
     pass_names = [k for k in stage_ms if k.startswith("pass_")]
-    pass_times = [t for k in pass_names for t in stage_ms[k]]
-    flops_pass = 2.0 * c.m * c.n * c.l
-    bytes_pass = 8.0 * (c.m * c.n + c.m * c.l + c.n * c.l)
+    pass_ms_loc = sum(t for k in pass_names for t in stage_ms[k])
+    pass_ms = max_over_ranks(pass_ms_loc, group, dev) if pass_names else 0.0
+    flops_pass = 2.0 * m_loc * c.n * c.l
+    bytes_pass = 8.0 * (m_loc * c.n + m_loc * c.l + c.n * c.l)
     roof = None
-    if pass_times:
-        mean_pass_ms = sum(pass_times) / stage_steps / passes(c)   # per width-l-equivalent pass
+    if pass_ms > 0:
+        mean_pass_ms = pass_ms / passes(c)
         ach = flops_pass / (mean_pass_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(ach / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": load_traffic(c.name),
+                "frac": round(ach / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": load_traffic(c.name) if world == 1 else None,
                 "kernel": "A-pass: FP64 DMMA GEMM gemm_tma_kernel (Y=AX and B=V^T A / A^T V, incl. split-K "
-                          "reduce); achieved = algorithmic A-pass flops / summed pass event time",
+                          "reduce); achieved = algorithmic A-pass flops / summed pass event time (per GPU)",
                 "algorithmic_flops_per_launch": flops_pass, "algorithmic_bytes_per_launch": bytes_pass,
-                "mean_pass_ms": round(mean_pass_ms, 4),
+                "mean_pass_ms": round(mean_pass_ms, 4), "apass_ms_per_step": round(pass_ms, 4),
                 "peak_source": "measured DMMA m8n8k4 FP64 microbenchmark (tools/microbench/fp64_peak.cu, "
                                "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
                 "hbm_frac": round(bytes_pass / (mean_pass_ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6540.8),
                                   4)}
-    apass_total_ms = sum(pass_times) / stage_steps if pass_times else None
+    # whole factorisation: the algorithmic A-pass flops of the step (the roofline-defining work)
+    # over the step time, against the N-GPU FP64 peak (BASELINE's "slower of bytes@8TB/s and flops@peak")
+    whole_flops = passes(c) * 2.0 * cg.m * c.n * c.l
+    t_roof_flop = whole_flops / (world * FP64_DMMA_PEAK_TFLOPS * 1e12)
+    t_roof_byte = passes(c) * 8.0 * (cg.m * c.n + cg.m * c.l + world * c.n * c.l) / (world * 8e12)
+    whole = {"flops": whole_flops, "t_roof_s": max(t_roof_flop, t_roof_byte), "bound": "tensor" if t_roof_flop >= t_roof_byte else "hbm",
+             "tflops": round(whole_flops / (ms_per_step * 1e-3) / 1e12, 3),
+             "frac": round(max(t_roof_flop, t_roof_byte) / (ms_per_step * 1e-3), 4)}
 
-    # ---- e2e through the public API with HOST buffers (pinned)
+    # ---- e2e through the public API with HOST buffers (pinned): rqlp_factorize copies this rank's
+    # rows of A host->device, factorises and copies Q, T, P back, all inside the timed call
     e2e = None
-    if not args.no_e2e and world == 1:
-        A_h = torch.empty(c.n, c.m, dtype=torch.float64, pin_memory=True).t()
-        A_h.copy_(A)
+    if not args.no_e2e:
         l = c.l
+        A_h = torch.empty(c.n, m_loc, dtype=torch.float64, pin_memory=True).t()
+        A_h.copy_(A)
         outs = tuple(torch.empty(cc, r, dtype=torch.float64, pin_memory=True).t()
-                     for r, cc in ((c.m, l), (l, l), (c.n, l)))
-        hh = rq.Handle(device=dev)
+                     for r, cc in ((m_loc, l), (l, l), (c.n, l)))
+        del A, out
+        torch.cuda.empty_cache()
+        hh = rq.Handle(device=dev, group=group)
         for _ in range(2):
             rq.factorize_host(A_h, c.k, c.p, q=c.q, d=c.d, b=c.b, seed=c.seed, handle=hh, out=outs)
         ts = []
-        for _ in range(max(3, min(args.steps, 10))):
-            torch.cuda.synchronize()
+        for _ in range(max(3, min(args.steps, 5))):
+            barrier()
             t0 = time.perf_counter()
             rq.factorize_host(A_h, c.k, c.p, q=c.q, d=c.d, b=c.b, seed=c.seed, handle=hh, out=outs)
             ts.append(time.perf_counter() - t0)
-        e2e = {"value": sum(ts) / len(ts), "unit": "s", "h2d_bytes_per_step": 8 * c.m * c.n,
-               "d2h_bytes_per_step": 8 * (c.m * l + l * l + c.n * l), "api": "rqlp_factorize (C ABI, pinned host)"}
+        e2e_s = max_over_ranks(sum(ts) / len(ts), group, dev)
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * cg.m * c.n,
+               "d2h_bytes_per_step": 8 * (cg.m * l + world * (l * l + c.n * l)),
+               "api": "rqlp_factorize (C ABI, pinned host buffers; max over ranks of the per-rank wall time)"}
         del hh
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        A_np = A.cpu().numpy()
-        sec, sample, th = oracle_time(A_np, c)
-        cpu = {"value": sec, "unit": "s", "cores": th, "kind": "oracle", "sample": sample}
+        def rows(ms):
+            return make_A_config(c, device=dev, row_range=(0, ms)).cpu().numpy()
+
+        sec, sample, th = oracle_time(rows, c)
+        cpu = {"value": sec, "unit": "s", "cores": th, "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+               "single_thread_s": single_thread_times()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic: A = U diag(sigma) V^T (+noise), Haar U, V from torch.linalg.qr of seeded "
                         "Gaussians; Omega from Philox4x64-10 (DESIGN.md §4)",
-                "config": {**describe(c), "global_m": cg.m, "parallelism": f"rows sharded over {world} rank(s)",
-                           "l2": "flushed between timed steps (256 MB write, untimed)",
-                           "apass_ms_per_step": apass_total_ms},
-                "apass_tflops": (passes(c) * flops_pass / (apass_total_ms * 1e-3) / 1e12) if apass_total_ms else None,
-                "tflops_effective": passes(c) * 2.0 * cg.m * c.n * c.l / (ms_per_step * 1e-3) / 1e12,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "config": config_dict(c, world, scaling, cg.m),
+                "apass_tflops_per_gpu": roof["achieved"] if roof else None,
+                "tflops_effective": whole["tflops"],
+                "roofline": roof, "roofline_whole_factorisation": whole, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(), "step_ms": [round(t, 4) for t in step_ms],
                 "stages_ms": {k: round(sum(v) / len(v), 4) for k, v in stage_ms.items()},
-                "device_flags": flags}
+                "replicated_outputs_identical": replicated_identical, "device_flags": flags}
         print(json.dumps(line), flush=True)
     if group is not None:
         torch.distributed.destroy_process_group()

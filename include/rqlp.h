@@ -2,8 +2,8 @@
  * rqlp.h -- C ABI of librqlp.so: B200-native (sm_100a) FP64 randomized QLP.
  *
  * Paper: N. Wu, H. Xiang, "Randomized QLP algorithm and error analysis", arXiv:1811.09334.
- * "PAPER.md:L" cites line L of the paper's LaTeX source (the upstream reference); readings
- * R1..R22 where the paper is silent, garbled or wrong are listed in DESIGN.md §3.
+ * "PAPER.md:L" cites line L of the paper's LaTeX source (the upstream reference); the readings
+ * (R1..R30) where the paper is silent, garbled or wrong are listed in DESIGN.md §3.
  *
  * Conventions (all entry points)
  *   - FP64 (IEEE binary64, round-to-nearest-even), column-major, leading dimension >= rows.
@@ -21,6 +21,11 @@
  *   - Errors (LAPACK style): 0 = success; -i = argument i illegal (checked before anything is
  *     enqueued); positive RQLP_ERR_* codes below for runtime failures.  Device-side numerical
  *     events (shifted CholeskyQR fallback taken) are not errors: rqlp_sync() reports them.
+ *   - Threads: calls on ONE handle are serialised by a per-handle lock (rqlp() shares one
+ *     default handle per device between all threads); different handles run concurrently.  The
+ *     device buffers a call reads or writes must not be used by other streams until the
+ *     handle's stream has passed the call (the Python binding orders the handle's stream against
+ *     torch's current stream on both sides of every call).
  */
 #ifndef RQLP_H
 #define RQLP_H
@@ -64,6 +69,18 @@ int rqlp_create(rqlp_handle_t *h, int device, void *cuda_stream);
 int rqlp_create_dist(rqlp_handle_t *h, int device, void *cuda_stream, const void *nccl_unique_id,
                      int rank, int nranks);
 int rqlp_get_unique_id(void *nccl_unique_id_out /* 128 bytes */);
+
+/* Create `nranks` (1..64) handles that act as the ranks of a row-sharded run INSIDE one process
+ * on ONE device (the multi-rank path testable on a single GPU).  handles_out
+ * receives nranks handles; all enqueue on `cuda_stream`.  Call the factorisations collectively
+ * exactly as with rqlp_create_dist handles -- one host thread per rank, each with its rank's row
+ * block of A and the same remaining arguments.  The ranks take turns (a host token ring) to
+ * enqueue their work on the shared stream, so the device runs the ranks' segments one after the
+ * other and no kernel ever waits for another rank; every sum over ranks adds the ranks' partials
+ * in fixed rank order, so the replicated outputs (L/T, P, pivots) are bit-identical on every
+ * rank.  A rank that fails (or whose call sequence diverges) aborts the group: the other ranks'
+ * calls return RQLP_ERR_NCCL (after at most 600 s).  Destroy every handle with rqlp_destroy. */
+int rqlp_create_loopback(rqlp_handle_t *handles_out, int nranks, int device, void *cuda_stream);
 int rqlp_destroy(rqlp_handle_t h);
 
 /* Bytes of device workspace the given call needs (m = local rows). */
@@ -104,8 +121,10 @@ int erqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
 
 /* Algorithm 3 + q deflated subspace iterations per block (reading R16):
  * block size 1 <= b <= l, h = ceil(l/b) blocks, ragged last block (reading R14);
- * Y_j = AΩ_j with the original A (line 3, reading R15), V_j = qr(Y_j), one block-CGS
- * re-orthogonalisation (eq. (18)), B_j = V_j^T A^(j-1) with A^(j-1) applied implicitly
+ * Y_j = AΩ_j with the original A (line 3, reading R15), V_j = qr(Y_j), the block-CGS
+ * re-orthogonalisation of eq. (18) applied twice (reading R28: "twice is enough" -- identical
+ * in exact arithmetic whenever V_j has a component outside span(V_<j)), B_j = V_j^T A^(j-1)
+ * with A^(j-1) applied implicitly
  * (A^(j-1) X = AX - V_<j (B_<j X), identical to eq. (19) in exact arithmetic), per-block
  * pivoted QLP of B_j, Q_j = V_j Q_B^(j), L = blkdiag(L_j) (lower), P = [P_1 .. P_h].
  * piv0[t] = global column of A, piv1[t] = index local to t's block. */
@@ -192,6 +211,14 @@ int rqlp_residual_sq(rqlp_handle_t h, int64_t m, int64_t n, int64_t l, const dou
  * rqlp_set_stage_outputs(h, NULL, 0, NULL, 0, NULL, 0) turns it off. */
 int rqlp_set_stage_outputs(rqlp_handle_t h, double *Y, int64_t ldy, double *V, int64_t ldv, double *B,
                            int64_t ldb);
+
+/* Power-step stage outputs (tests; staged parity of every A-pass at full size): subsequent
+ * factorisations on h copy, for power iteration it (0..q-1), V before the step (m x l), its A-pass
+ * result Z = A^T V (n x l; BRQLP: the deflated A^(j-1)^T V_j), W = orth(Z) (n x l) and the A-pass
+ * result Y = A W (m x l; BRQLP: deflated) into columns it*l .. it*l+l-1 of these buffers (BRQLP:
+ * block j's columns it*l + c0_j ..).  Buffers are m x (q l) / n x (q l).  NULL turns one off. */
+int rqlp_set_power_stage_outputs(rqlp_handle_t h, double *Vpre, int64_t ldvp, double *Z, int64_t ldz, double *W,
+                                 int64_t ldw, double *Ypow, int64_t ldyp);
 
 /* Per-stage device timings (ms) of the last factorisation when timing is enabled:
  * names/values written up to *count entries; returns number available. */

@@ -73,6 +73,7 @@ def lib():
         L.orc_residual.argtypes = [_i64, _i64, _i64, _d, _i64, _d, _i64, _d, _i64, _d, _i64]
         L.orc_residual.restype = ctypes.c_double
         L.orc_num_threads.restype = _int
+        L.orc_set_num_threads.argtypes = [_int]
     return _lib
 
 
@@ -91,6 +92,11 @@ def _ld(a):
 
 def num_threads() -> int:
     return lib().orc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the following oracle calls (bench.py's single-thread sample)."""
+    lib().orc_set_num_threads(int(n))
 
 
 # ---------------- RNG ----------------

@@ -27,6 +27,15 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* Thread count of the following calls (bench.py's single-thread cpu_baseline sample); no arithmetic. */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 /* ======================================================================================
  * Ω generator.  DESIGN.md §4: Philox4x64-10 (Salmon et al. SC'11), key = (seed, 0),
  * counter = (block, stream, 0, 0); uniforms u(x) = ((x>>12)+0.5)*2^-52; Box-Muller with both

@@ -102,6 +102,7 @@ double orc_residual(int64_t m, int64_t n, int64_t l, const double *A, int64_t ld
                     const double *P, int64_t ldp);
 
 int orc_num_threads(void);
+void orc_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

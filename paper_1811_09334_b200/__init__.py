@@ -97,6 +97,25 @@ class Handle:
         self.group = group
 
     @classmethod
+    def loopback(cls, nranks: int, device=None, stream=None) -> list["Handle"]:
+        """`nranks` virtual ranks of a row-sharded run in THIS process on ONE GPU
+        (rqlp_create_loopback): one handle per rank, all on one stream.  Call the factorisations
+        collectively, one host thread per rank, each with its rank's row block of A; the sums over
+        ranks run in fixed rank order (bit-identical replicated outputs)."""
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+        stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        arr = (ctypes.c_void_p * nranks)()
+        _check(lib().rqlp_create_loopback(arr, nranks, dev.index, ctypes.c_void_p(stream.cuda_stream)),
+               "rqlp_create_loopback")
+        hs = []
+        for r in range(nranks):
+            h = cls.__new__(cls)
+            h.device, h.stream, h.h, h._ws, h.group = dev, stream, ctypes.c_void_p(arr[r]), None, None
+            h.rank, h.nranks = r, nranks
+            hs.append(h)
+        return hs
+
+    @classmethod
     def default(cls, device=None) -> "Handle":
         dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
         stream = torch.cuda.current_stream(dev)
@@ -148,6 +167,13 @@ class Handle:
                                             _ld(V) if V is not None else 0, _ptr(B),
                                             _ld(B) if B is not None else 0), "rqlp_set_stage_outputs")
 
+    def set_power_stage_outputs(self, Vpre=None, Z=None, W=None, Ypow=None):
+        """Tests: copy each power step's V (before), Z = A^T V, W = orth(Z) and Y = A W of subsequent
+        factorisations (iteration it at columns it*l ..; see rqlp.h)."""
+        ld = lambda t: _ld(t) if t is not None else 0  # noqa: E731
+        _check(lib().rqlp_set_power_stage_outputs(self.h, _ptr(Vpre), ld(Vpre), _ptr(Z), ld(Z), _ptr(W), ld(W),
+                                                  _ptr(Ypow), ld(Ypow)), "rqlp_set_power_stage_outputs")
+
     def launches(self) -> int:
         return int(lib().rqlp_launch_count(self.h))
 
@@ -161,6 +187,28 @@ class Handle:
 
 def _handle(handle):
     return handle if handle is not None else Handle.default()
+
+
+class _ordered:
+    """Stream ordering between torch's current stream and the handle's stream: the library's work
+    starts after everything already enqueued on the current stream (inputs, the outputs' and the
+    workspace's allocations) and the current stream waits for the library's work before it uses
+    the outputs or lets the caching allocator recycle any of these buffers."""
+
+    def __init__(self, h: "Handle"):
+        self.h = h
+
+    def __enter__(self):
+        self.cur = torch.cuda.current_stream(self.h.device)
+        self.same = self.cur.cuda_stream == self.h.stream.cuda_stream
+        if not self.same:
+            self.h.stream.wait_stream(self.cur)
+        return self
+
+    def __exit__(self, *exc):
+        if not self.same:
+            self.cur.wait_stream(self.h.stream)
+        return False
 
 
 def _outputs(m: int, n: int, l: int, npiv: int, device):
@@ -186,8 +234,9 @@ def rqlp(A: torch.Tensor, k: int, p: int, q: int = 0, seed: int = 0, handle: Han
     l = k + p
     h.workspace(VARIANT_RQLP, m, n, k, p, q, 0, 0)
     Q, L, P, piv0, piv1 = _outputs(m, n, l, 2, A.device)
-    _check(lib().rqlp_ex(h.h, m, n, k, p, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
-                         _ptr(piv0), _ptr(piv1)), "rqlp_ex")
+    with _ordered(h):
+        _check(lib().rqlp_ex(h.h, m, n, k, p, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
+                             _ptr(piv0), _ptr(piv1)), "rqlp_ex")
     return Q, L, P, piv0, piv1
 
 
@@ -201,8 +250,9 @@ def erqlp(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 2, seed: int = 0
     h.workspace(VARIANT_ERQLP, m, n, k, p, q, d, 0)
     Q, T, P, piv0 = _outputs(m, n, l, 1, A.device)
     tu = ctypes.c_int(0)
-    _check(lib().erqlp_ex(h.h, m, n, k, p, q, d, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(T), _ld(T),
-                          ctypes.byref(tu), _ptr(P), _ld(P), _ptr(piv0)), "erqlp_ex")
+    with _ordered(h):
+        _check(lib().erqlp_ex(h.h, m, n, k, p, q, d, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(T), _ld(T),
+                              ctypes.byref(tu), _ptr(P), _ld(P), _ptr(piv0)), "erqlp_ex")
     return Q, T, P, piv0, bool(tu.value)
 
 
@@ -214,8 +264,9 @@ def brqlp(A: torch.Tensor, k: int, p: int, b: int, q: int = 0, seed: int = 0, ha
     l = k + p
     h.workspace(VARIANT_BRQLP, m, n, k, p, q, 0, b)
     Q, L, P, piv0, piv1 = _outputs(m, n, l, 2, A.device)
-    _check(lib().brqlp_ex(h.h, m, n, k, p, b, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P),
-                          _ld(P), _ptr(piv0), _ptr(piv1)), "brqlp_ex")
+    with _ordered(h):
+        _check(lib().brqlp_ex(h.h, m, n, k, p, b, q, _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P),
+                              _ld(P), _ptr(piv0), _ptr(piv1)), "brqlp_ex")
     return Q, L, P, piv0, piv1
 
 
@@ -259,7 +310,8 @@ def rqlp_host(A, k: int, p: int, q: int = 0, seed: int = 0):
 def omega(n: int, l: int, seed: int, device="cuda", handle=None) -> torch.Tensor:
     h = _handle(handle)
     Om = cm_empty(n, l, device)
-    _check(lib().rqlp_omega(h.h, n, l, seed, _ptr(Om), _ld(Om)), "rqlp_omega")
+    with _ordered(h):
+        _check(lib().rqlp_omega(h.h, n, l, seed, _ptr(Om), _ld(Om)), "rqlp_omega")
     return Om
 
 
@@ -268,8 +320,9 @@ def gemm_nn(A, X, handle=None) -> torch.Tensor:
     h = _handle(handle)
     h.clear_workspace()
     Y = cm_empty(A.shape[0], X.shape[1], A.device)
-    _check(lib().rqlp_gemm_nn(h.h, A.shape[0], X.shape[1], A.shape[1], _ptr(A), _ld(A), _ptr(X), _ld(X), _ptr(Y),
-                              _ld(Y)), "rqlp_gemm_nn")
+    with _ordered(h):
+        _check(lib().rqlp_gemm_nn(h.h, A.shape[0], X.shape[1], A.shape[1], _ptr(A), _ld(A), _ptr(X), _ld(X), _ptr(Y),
+                                  _ld(Y)), "rqlp_gemm_nn")
     return Y
 
 
@@ -280,8 +333,9 @@ def gemm_tn(A, V, trans_out: bool = False, handle=None) -> torch.Tensor:
     m, kk = A.shape
     c = V.shape[1]
     Z = cm_empty(c, kk, A.device) if trans_out else cm_empty(kk, c, A.device)
-    _check(lib().rqlp_gemm_tn(h.h, m, c, kk, _ptr(A), _ld(A), _ptr(V), _ld(V), _ptr(Z), _ld(Z),
-                              1 if trans_out else 0), "rqlp_gemm_tn")
+    with _ordered(h):
+        _check(lib().rqlp_gemm_tn(h.h, m, c, kk, _ptr(A), _ld(A), _ptr(V), _ld(V), _ptr(Z), _ld(Z),
+                                  1 if trans_out else 0), "rqlp_gemm_tn")
     return Z
 
 
@@ -292,8 +346,9 @@ def orth(Y, return_r: bool = False, handle=None):
     m, c = Y.shape
     V = cm_empty(m, c, Y.device)
     R = cm_empty(c, c, Y.device) if return_r else None
-    _check(lib().rqlp_orth(h.h, m, c, _ptr(Y), _ld(Y), _ptr(V), _ld(V), _ptr(R), _ld(R) if R is not None else 1),
-           "rqlp_orth")
+    with _ordered(h):
+        _check(lib().rqlp_orth(h.h, m, c, _ptr(Y), _ld(Y), _ptr(V), _ld(V), _ptr(R), _ld(R) if R is not None else 1),
+               "rqlp_orth")
     return (V, R) if return_r else V
 
 
@@ -305,7 +360,8 @@ def cpqr(M, handle=None):
     s = min(r, c)
     Q, R = cm_empty(r, s, M.device), cm_empty(s, c, M.device)
     perm = torch.empty(c, dtype=torch.int64, device=M.device)
-    _check(lib().rqlp_cpqr(h.h, r, c, _ptr(M), _ld(M), _ptr(Q), _ld(Q), _ptr(R), _ld(R), _ptr(perm)), "rqlp_cpqr")
+    with _ordered(h):
+        _check(lib().rqlp_cpqr(h.h, r, c, _ptr(M), _ld(M), _ptr(Q), _ld(Q), _ptr(R), _ld(R), _ptr(perm)), "rqlp_cpqr")
     return Q, R, perm
 
 
@@ -318,8 +374,9 @@ def qlp_tail(B, d: int = 0, handle=None) -> dict:
     piv0 = torch.empty(l, dtype=torch.int64, device=B.device)
     piv1 = torch.empty(l, dtype=torch.int64, device=B.device)
     tu = ctypes.c_int(0)
-    _check(lib().rqlp_qlp_tail(h.h, l, n, _ptr(B), _ld(B), d, _ptr(QB), _ld(QB), _ptr(T), _ld(T), _ptr(PB), _ld(PB),
-                               _ptr(piv0), _ptr(piv1), ctypes.byref(tu)), "rqlp_qlp_tail")
+    with _ordered(h):
+        _check(lib().rqlp_qlp_tail(h.h, l, n, _ptr(B), _ld(B), d, _ptr(QB), _ld(QB), _ptr(T), _ld(T), _ptr(PB), _ld(PB),
+                                   _ptr(piv0), _ptr(piv1), ctypes.byref(tu)), "rqlp_qlp_tail")
     return dict(QB=QB, T=T, PB=PB, piv0=piv0, piv1=piv1, t_is_upper=bool(tu.value))
 
 
@@ -331,8 +388,9 @@ def residual(A, Q, T, P, handle=None) -> float:
     out = torch.zeros(1, dtype=torch.float64, device=A.device)
     m, n = A.shape
     l = Q.shape[1]
-    _check(lib().rqlp_residual_sq(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(T), _ld(T), _ptr(P), _ld(P),
-                                  _ptr(out)), "rqlp_residual_sq")
+    with _ordered(h):
+        _check(lib().rqlp_residual_sq(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(T), _ld(T), _ptr(P), _ld(P),
+                                      _ptr(out)), "rqlp_residual_sq")
     return float(out.item()) ** 0.5
 
 
@@ -371,8 +429,9 @@ def factorize_host(A: torch.Tensor, k: int, p: int, q: int = 0, d: int = 0, b: i
     Q, T, P = out
     tu = ctypes.c_int(0)
     h.clear_workspace()
-    _check(lib().rqlp_factorize(h.h, variant, m, n, k, p, q, d, b or 0, _ptr(A), _ld(A), seed, _ptr(Q), _ptr(T),
-                                _ptr(P), ctypes.byref(tu)), "rqlp_factorize")
+    with _ordered(h):
+        _check(lib().rqlp_factorize(h.h, variant, m, n, k, p, q, d, b or 0, _ptr(A), _ld(A), seed, _ptr(Q), _ptr(T),
+                                    _ptr(P), ctypes.byref(tu)), "rqlp_factorize")
     return Q, T, P, bool(tu.value)
 
 
@@ -389,9 +448,10 @@ def autorank(A: torch.Tensor, b: int, l_max: int, eps: float, q: int = 0, seed: 
     piv0 = torch.empty(l_max, dtype=torch.int64, device=A.device)
     piv1 = torch.empty(l_max, dtype=torch.int64, device=A.device)
     lo, err = ctypes.c_int(0), ctypes.c_double(0.0)
-    _check(lib().rqlp_autorank_ex(h.h, m, n, b, l_max, q, float(eps), _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L),
-                                  _ld(L), _ptr(P), _ld(P), _ptr(piv0), _ptr(piv1), ctypes.byref(lo),
-                                  ctypes.byref(err)), "rqlp_autorank_ex")
+    with _ordered(h):
+        _check(lib().rqlp_autorank_ex(h.h, m, n, b, l_max, q, float(eps), _ptr(A), _ld(A), seed, _ptr(Q), _ld(Q), _ptr(L),
+                                      _ld(L), _ptr(P), _ld(P), _ptr(piv0), _ptr(piv1), ctypes.byref(lo),
+                                      ctypes.byref(err)), "rqlp_autorank_ex")
     l = lo.value
     return dict(Q=Q[:, :l], T=L[:l, :l], P=P[:, :l], piv0=piv0[:l], piv1=piv1[:l], l=l, err=err.value)
 
@@ -406,6 +466,7 @@ def tqlp(A: torch.Tensor, l: int, handle: Handle | None = None) -> dict:
     Q, L, P = cm_empty(m, l, A.device), cm_empty(l, l, A.device), cm_empty(n, l, A.device)
     piv0 = torch.empty(l, dtype=torch.int64, device=A.device)
     piv1 = torch.empty(l, dtype=torch.int64, device=A.device)
-    _check(lib().rqlp_tqlp_ex(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
-                              _ptr(piv0), _ptr(piv1)), "rqlp_tqlp_ex")
+    with _ordered(h):
+        _check(lib().rqlp_tqlp_ex(h.h, m, n, l, _ptr(A), _ld(A), _ptr(Q), _ld(Q), _ptr(L), _ld(L), _ptr(P), _ld(P),
+                                  _ptr(piv0), _ptr(piv1)), "rqlp_tqlp_ex")
     return dict(Q=Q, T=L, P=P, piv0=piv0, piv1=piv1, t_is_upper=False)

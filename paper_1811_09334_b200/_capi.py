@@ -18,6 +18,7 @@ SIGNATURES = [
     ("rqlp_create", _int, [ctypes.POINTER(_vp), _int, _vp]),
     ("rqlp_create_dist", _int, [ctypes.POINTER(_vp), _int, _vp, _vp, _int, _int]),
     ("rqlp_get_unique_id", _int, [_vp]),
+    ("rqlp_create_loopback", _int, [ctypes.POINTER(_vp), _int, _int, _vp]),
     ("rqlp_destroy", _int, [_vp]),
     ("rqlp_workspace_size", _int, [_vp, _int, _i64, _i64, _int, _int, _int, _int, _int, ctypes.POINTER(_sz)]),
     ("rqlp_set_workspace", _int, [_vp, _vp, _sz]),
@@ -44,6 +45,7 @@ SIGNATURES = [
                              ctypes.POINTER(_int)]),
     ("rqlp_residual_sq", _int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     ("rqlp_set_stage_outputs", _int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64]),
+    ("rqlp_set_power_stage_outputs", _int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     ("rqlp_set_timing", _int, [_vp, _int]),
     ("rqlp_get_timing", _int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _int]),
     ("rqlp_launch_count", _i64, [_vp]),

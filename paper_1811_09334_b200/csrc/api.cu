@@ -12,6 +12,7 @@
 
 struct rqlp_handle_s {
   int magic = 0x51504c52;
+  std::recursive_mutex mu;  // calls on one handle are serialised (the default handle is shared)
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
@@ -33,6 +34,10 @@ struct rqlp_handle_s {
   // optional stage outputs (tests): sketch Y, final V, projected B
   double *dbgY = nullptr, *dbgV = nullptr, *dbgB = nullptr;
   int64_t ldY = 0, ldV = 0, ldB = 0;
+  // power-step stage outputs (tests): V before each power step, its A-pass results Z = A^T V and
+  // Y = A W (deflated for BRQLP) and W = orth(Z); iteration `it` at columns it*l (+ block offset)
+  double *dbgVP = nullptr, *dbgZ = nullptr, *dbgW = nullptr, *dbgYP = nullptr;
+  int64_t ldVP = 0, ldZ = 0, ldW = 0, ldYP = 0;
   // CUDA-graph cache: a factorisation is captured on its second call with the same shape,
   // pointers and workspace, then replayed (one graph launch instead of ~100-300 kernel launches)
   struct GEntry {
@@ -297,24 +302,33 @@ struct WsError : std::runtime_error {
 };
 
 template <typename F>
-int guarded(rqlp_handle_t h, F f) {
+int guarded(rqlp_handle_t h, F f, bool collective = false) {
   if (!valid(h)) return RQLP_ERR_HANDLE;
+  std::lock_guard<std::recursive_mutex> lock(h->mu);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != h->device) cudaSetDevice(h->device);
   int rc = RQLP_OK;
+  bool began = false;
   try {
+    if (collective) {
+      comm_call_begin(h->comm);   // loopback ranks: wait for this rank's turn
+      began = true;
+    }
     rc = f();
   } catch (const CudaError &e) {
     fprintf(stderr, "[rqlp] CUDA error: %s\n", e.what());
     rc = RQLP_ERR_CUDA;
+  } catch (const NcclError &e) {
+    fprintf(stderr, "[rqlp] NCCL/loopback error: %s\n", e.what());
+    rc = RQLP_ERR_NCCL;
   } catch (const std::exception &e) {
     std::string w = e.what();
     if (w.find("workspace") != std::string::npos) rc = RQLP_ERR_WORKSPACE;
-    else if (w.find("nccl") != std::string::npos || w.find("NCCL") != std::string::npos) rc = RQLP_ERR_NCCL;
     else rc = RQLP_ERR_INTERNAL;
     fprintf(stderr, "[rqlp] error: %s\n", e.what());
   }
+  if (collective) comm_call_end(h->comm, rc != RQLP_OK || !began);
   if (prev != h->device) cudaSetDevice(prev);
   return rc;
 }
@@ -346,13 +360,17 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh, q > 0);
   c.mark("orth");
   for (int it = 0; it < q; ++it) {
+    if (h->dbgVP) launch_copy(c, m, l, P.V, P.ldm, h->dbgVP + it * l * h->ldVP, h->ldVP, false);
     gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.Z, P.ldn, false, P.part, P.part_elems); // Z = A^T V
     allreduce_sum(c, P.Z, P.ldn * l);
     c.mark("pass_power_AtV");
+    if (h->dbgZ) launch_copy(c, n, l, P.Z, P.ldn, h->dbgZ + it * l * h->ldZ, h->ldZ, false);
     orth(c, P.orth, n, l, P.Z, P.ldn, P.W, P.ldn, nullptr, 0, false, true);           // W = qr(Z) (span)
     c.mark("orth");
+    if (h->dbgW) launch_copy(c, n, l, P.W, P.ldn, h->dbgW + it * l * h->ldW, h->ldW, false);
     gemm_nn(c, m, l, n, A, lda, P.W, P.ldn, P.Y, P.ldm, P.part, P.part_elems);        // Y = A W
     c.mark("pass_power_AW");
+    if (h->dbgYP) launch_copy(c, m, l, P.Y, P.ldm, h->dbgYP + it * l * h->ldYP, h->ldYP, false);
     orth(c, P.orth, m, l, P.Y, P.ldm, P.V, P.ldm, nullptr, 0, sh, it + 1 < q);        // V = qr(Y)
     c.mark("orth");
   }
@@ -370,8 +388,10 @@ int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
   const int variant = d > 0 ? RQLP_VARIANT_ERQLP : RQLP_VARIANT_RQLP;
   const size_t need = plan_bytes(variant, m, n, l, 0, h->num_sms);
   char *ws = get_ws(h, need, allow_own);
-  const std::string key = make_key(h, "rqlp", {m, n, k, p, q, d, lda, (int64_t)seed, ldq, ldt, ldp, h->ldY, h->ldV, h->ldB},
-                                   {A, Q, T, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB});
+  const std::string key = make_key(h, "rqlp", {m, n, k, p, q, d, lda, (int64_t)seed, ldq, ldt, ldp, h->ldY, h->ldV, h->ldB,
+                                    h->ldVP, h->ldZ, h->ldW, h->ldYP},
+                                   {A, Q, T, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB, h->dbgVP, h->dbgZ, h->dbgW,
+                                    h->dbgYP});
   return with_graph(h, key, [&](Ctx &c) {
     Arena a;
     a.base = ws;
@@ -405,8 +425,10 @@ int run_brqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q,
   const int64_t l = (int64_t)k + p;
   const size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l, b, h->num_sms);
   char *ws = get_ws(h, need, allow_own);
-  const std::string key = make_key(h, "brqlp", {m, n, k, p, b, q, lda, (int64_t)seed, ldq, ldl, ldp, h->ldY, h->ldV, h->ldB},
-                                   {A, Q, L, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB});
+  const std::string key = make_key(h, "brqlp", {m, n, k, p, b, q, lda, (int64_t)seed, ldq, ldl, ldp, h->ldY, h->ldV, h->ldB,
+                                    h->ldVP, h->ldZ, h->ldW, h->ldYP},
+                                   {A, Q, L, Pout, piv0, piv1, ws, h->dbgY, h->dbgV, h->dbgB, h->dbgVP, h->dbgZ, h->dbgW,
+                                    h->dbgYP});
   return with_graph(h, key, [&](Ctx &c) { enqueue_brqlp(c, h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, Pout,
                                                         ldp, piv0, piv1, ws, need); });
 }
@@ -489,6 +511,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
       reorth(c0, bj);                                                                      // l.5
       for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
+        if (h->dbgVP) launch_copy(c, m, bj, Vj, ldm, h->dbgVP + (it * l + c0) * h->ldVP, h->ldVP, false);
         c.mark("b_other");
         gemm_tn(c, m, bj, n, A, lda, Vj, ldm, P.Z, ldn, false, P.part, P.part_elems);     // Z = A^T Vj
         allreduce_sum(c, P.Z, ldn * bj);
@@ -499,7 +522,9 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
           gemm_generic_ex(c, true, false, n, bj, c0, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems, false,
                           nullptr, 0);                                                     // Z -= B_<j^T C
         }
+        if (h->dbgZ) launch_copy(c, n, bj, P.Z, ldn, h->dbgZ + (it * l + c0) * h->ldZ, h->ldZ, false);
         orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
+        if (h->dbgW) launch_copy(c, n, bj, P.W, ldn, h->dbgW + (it * l + c0) * h->ldW, h->ldW, false);
         c.mark("b_other");
         gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
         c.mark("pass_block_AW");
@@ -509,6 +534,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
           gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part,
                           P.part_elems, false, nullptr, 0);                                // Y -= V_<j D
         }
+        if (h->dbgYP) launch_copy(c, m, bj, P.Y + c0 * ldm, ldm, h->dbgYP + (it * l + c0) * h->ldYP, h->ldYP, false);
         orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
         reorth(c0, bj);
       }
@@ -670,6 +696,26 @@ int rqlp_create_dist(rqlp_handle_t *out, int device, void *cuda_stream, const vo
   return RQLP_OK;
 }
 
+int rqlp_create_loopback(rqlp_handle_t *out, int nranks, int device, void *cuda_stream) {
+  if (!out) return -1;
+  if (nranks < 1 || nranks > 64) return -2;
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  void *group = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    int rc = rqlp_create(&out[r], device, cuda_stream);
+    if (rc != RQLP_OK) {
+      for (int i = 0; i < r; ++i) rqlp_destroy(out[i]);
+      for (int i = 0; i < nranks; ++i) out[i] = nullptr;
+      return rc;
+    }
+    if (!group) group = comm_loopback_group(nranks, device, (cudaStream_t)cuda_stream);
+    out[r]->rank = r;
+    out[r]->nranks = nranks;
+    out[r]->comm = comm_loopback_init(group, r);
+  }
+  return RQLP_OK;
+}
+
 int rqlp_destroy(rqlp_handle_t h) {
   if (!valid(h)) return RQLP_ERR_HANDLE;
   int prev = 0;
@@ -735,7 +781,7 @@ int rqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, const do
   if (ldp < n) return -15;
   return guarded(h, [&] {
     return run_rqlp(h, m, n, k, p, q, 0, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
-  });
+  }, true);
 }
 
 int erqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, const double *A, int64_t lda,
@@ -758,7 +804,7 @@ int erqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
   if (t_is_upper) *t_is_upper = (d % 2 == 0) ? 1 : 0;
   return guarded(h, [&] {
     return run_rqlp(h, m, n, k, p, q, d, A, lda, seed, Q, ldq, T, ldt, P, ldp, piv0, nullptr, true);
-  });
+  }, true);
 }
 
 int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A, int64_t lda,
@@ -781,7 +827,7 @@ int brqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, 
   if (ldp < n) return -16;
   return guarded(h, [&] {
     return run_brqlp(h, m, n, k, p, b, q, A, lda, seed, Q, ldq, L, ldl, P, ldp, piv0, piv1, true);
-  });
+  }, true);
 }
 
 int rqlp_tqlp_ex(rqlp_handle_t h, int64_t m, int64_t n, int l, const double *A, int64_t lda, double *Q, int64_t ldq,
@@ -837,7 +883,7 @@ int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, in
     *l_out = ar.l_out;
     if (err_out) *err_out = ar.err;
     return RQLP_OK;
-  });
+  }, true);
 }
 
 static bool is_device_ptr(const void *p) {
@@ -893,7 +939,7 @@ static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int
     if (!dP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
     RQLP_CUDA(cudaStreamSynchronize(h->stream));
     return RQLP_OK;
-  });
+  }, true);
 }
 
 int rqlp_factorize(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
@@ -943,6 +989,8 @@ int rqlp(int64_t m, int64_t n, int k, int p, int q, const double *A, int64_t lda
 int rqlp_sync(rqlp_handle_t h, unsigned *flags) {
   return guarded(h, [&] {
     RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    if (int ae = comm_async_error(h->comm))   // NCCL asynchronous failure (ncclCommGetAsyncError)
+      throw NcclError("ncclCommGetAsyncError: " + std::to_string(ae));
     if (flags) {
       unsigned f = 0;
       RQLP_CUDA(cudaMemcpy(&f, h->dflags + FLAG_WORD, sizeof(unsigned), cudaMemcpyDeviceToHost));
@@ -1154,6 +1202,16 @@ int rqlp_set_stage_outputs(rqlp_handle_t h, double *Y, int64_t ldy, double *V, i
   h->dbgY = Y; h->ldY = ldy;
   h->dbgV = V; h->ldV = ldv;
   h->dbgB = B; h->ldB = ldb;
+  return RQLP_OK;
+}
+
+int rqlp_set_power_stage_outputs(rqlp_handle_t h, double *Vpre, int64_t ldvp, double *Z, int64_t ldz, double *W,
+                                 int64_t ldw, double *Ypow, int64_t ldyp) {
+  if (!valid(h)) return RQLP_ERR_HANDLE;
+  h->dbgVP = Vpre; h->ldVP = ldvp;
+  h->dbgZ = Z; h->ldZ = ldz;
+  h->dbgW = W; h->ldW = ldw;
+  h->dbgYP = Ypow; h->ldYP = ldyp;
   return RQLP_OK;
 }
 

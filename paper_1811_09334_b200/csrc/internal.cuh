@@ -139,10 +139,21 @@ struct Ctx {
   }
 };
 
-// ---- NCCL (comm.cu) ----
+// ---- exchange steps of row-sharded runs (comm.cu): NCCL or in-process loopback ranks ----
+enum CommKind : int { COMM_NONE = 0, COMM_NCCL = 1, COMM_LOOPBACK = 2 };
+struct NcclError : std::runtime_error {  // NCCL / loopback failures -> RQLP_ERR_NCCL
+  using std::runtime_error::runtime_error;
+};
 int comm_unique_id(void *out);
 void *comm_init(const void *uid, int rank, int nranks);
+void *comm_loopback_group(int nranks, int device, cudaStream_t stream);
+void *comm_loopback_init(void *group, int rank);
+int comm_kind(void *comm);
 void comm_destroy(void *comm);
+int comm_async_error(void *comm);
+// loopback ranks enqueue a factorisation only while they hold the group's turn
+void comm_call_begin(void *comm);
+void comm_call_end(void *comm, bool failed);
 void allreduce_sum(Ctx &c, double *buf, int64_t count);
 
 // Bump allocator over a workspace; base == nullptr measures only.

@@ -106,15 +106,17 @@ def make_A(m: int, n: int, sig: torch.Tensor, rank: int | None = None, noise: fl
         torch.matmul(Vs, Ul[c0:c1].t(), out=At[:, c0:c1])
     if noise != 0.0:
         gn = torch.Generator(device=dev)
-        gn.manual_seed(int(seed) * 104729 + 3)
-        # noise rows are generated in fixed global chunks so a shard's bits do not depend on sharding
+        # noise rows are generated in fixed global chunks, each from its own seed, so a shard's bits
+        # do not depend on the sharding and a row block never generates the other blocks' noise
         scale = noise / math.sqrt(n)
         for g0 in range(0, m, chunk):
             g1 = min(m, g0 + chunk)
-            G = torch.randn(n, g1 - g0, generator=gn, dtype=torch.float64, device=dev)
             a0, a1 = max(g0, r0), min(g1, r1)
-            if a0 < a1:
-                At[:, a0 - r0:a1 - r0].add_(G[:, a0 - g0:a1 - g0], alpha=scale)
+            if a0 >= a1:
+                continue
+            gn.manual_seed(int(seed) * 104729 + 3 + 7 * (g0 // chunk))
+            G = torch.randn(n, g1 - g0, generator=gn, dtype=torch.float64, device=dev)
+            At[:, a0 - r0:a1 - r0].add_(G[:, a0 - g0:a1 - g0], alpha=scale)
             del G
     return col_major(At)
 

@@ -7,6 +7,7 @@ Per-stage GEMM tolerances: |ΔY_ij| <= 64 u k (|A||X|)_ij.
 import numpy as np
 import pytest
 import torch
+from parity import check_factorization
 
 pytestmark = pytest.mark.gpu
 
@@ -160,22 +161,10 @@ def test_qlp_tail_parity(rq, orc, d, l, n):
 
 
 # ------------------------------------------------------------------ end to end
-def _check_factorization(rq, orc, A, g, o, l, sig_ratio=None):
-    """north_star tolerances."""
-    An = np.linalg.norm(A)
-    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), "piv0 differ"
-    if g.get("piv1") is not None:
-        assert np.array_equal(g["piv1"].cpu().numpy(), o["piv1"]), "piv1 differ"
-    Lg, Lo = np.diag(_np(g["T"])), np.diag(o["T"])
-    mask = np.ones(l, bool) if sig_ratio is None else sig_ratio >= 1e-8
-    rel = np.abs(Lg - Lo)[mask] / np.abs(Lo)[mask]
-    assert rel.max() <= 1e-10, f"L-values rel diff {rel.max()}"
-    Qg, Pg, Tg = _np(g["Q"]), _np(g["P"]), _np(g["T"])
-    rg = orc.residual(A, Qg, Tg, Pg) / An
-    ro = orc.residual(A, o["Q"], o["T"], o["P"]) / An
-    assert abs(rg - ro) <= 1e-12, (rg, ro)
-    assert np.abs(Qg.T @ Qg - np.eye(l)).max() <= 1e-13 * l
-    return rg, ro
+def _check_factorization(rq, orc, A, g, o, l, sig_ratio=None, block=None, B_oracle=None, tag=""):
+    """north_star tolerances plus element-wise Q, T, P and P^T P (tests/parity.py)."""
+    rec = check_factorization(orc, A, g, o, l, sig_ratio=sig_ratio, block=block, B_oracle=B_oracle, tag=tag)
+    return rec["res_gpu"], rec["res_orc"]
 
 
 CASES = [  # (name, m, n, k, p, q, d, sigma)
@@ -200,10 +189,10 @@ def test_end_to_end_parity(rq, orc, case):
     A = _rand_svd(m, n, sig, m + n)
     l = k + p
     g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=7)
-    o = orc.rqlp(A, k, p, q=q, d=d, seed=7)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=7, stages=True)
     if d >= 1:
         o["piv1"] = None
-    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0])
+    _check_factorization(rq, orc, A, g, o, l, sig[:l] / sig[0], B_oracle=o["B"], tag=name)
 
 
 @pytest.mark.parametrize("b,q", [(64, 1), (7, 0), (16, 1), (136, 0)])
@@ -212,8 +201,8 @@ def test_brqlp_parity(rq, orc, b, q):
     sig = np.exp(-np.arange(1, 701.0) / 100)
     A = _rand_svd(m, n, sig, 99)
     g = rq.factorize(_cm(A), k, p, q=q, b=b, seed=4)
-    o = orc.brqlp(A, k, p, b=b, q=q, seed=4)
-    _check_factorization(rq, orc, A, g, o, k + p)
+    o = orc.brqlp(A, k, p, b=b, q=q, seed=4, stages=True)
+    _check_factorization(rq, orc, A, g, o, k + p, block=b, B_oracle=o["V"].T @ A, tag=f"brqlp b={b} q={q}")
 
 
 def test_residual_kernel(rq, orc):
@@ -285,7 +274,7 @@ def test_brqlp_unit_blocks(rq, orc):
     A = _rand_svd(200, 120, np.exp(-np.arange(1, 121.0) / 10), 31)
     g = rq.factorize(_cm(A), 6, 3, q=1, b=1, seed=2)
     o = orc.brqlp(A, 6, 3, b=1, q=1, seed=2)
-    _check_factorization(rq, orc, A, g, o, 9)
+    _check_factorization(rq, orc, A, g, o, 9, block=1)
 
 
 def test_argument_errors_gpu(rq):
@@ -336,7 +325,7 @@ def test_autorank_parity(rq, orc, m, n, b, l_max, eps, q):
     o = orc.autorank(A, b=b, l_max=l_max, eps=eps, q=q, seed=6)
     assert g["l"] == o["l"], (g["l"], o["l"])
     l = g["l"]
-    _check_factorization(rq, orc, A, g, o, l)
+    _check_factorization(rq, orc, A, g, o, l, block=b)
     assert g["err"] == pytest.approx(o["err"], rel=1e-8, abs=1e-13)
     direct = orc.residual(A, _np(g["Q"]), _np(g["T"]), _np(g["P"])) / np.linalg.norm(A)
     assert g["err"] == pytest.approx(direct, rel=1e-6, abs=1e-13)
@@ -392,7 +381,7 @@ def test_brqlp_q0_two_passes(rq, orc):
     finally:
         h.set_timing(False)
     o = orc.brqlp(A, k, p, b=b, q=0, seed=9)
-    _check_factorization(rq, orc, A, g, o, k + p)
+    _check_factorization(rq, orc, A, g, o, k + p, block=b)
     passes = [nm for nm in names if nm.startswith("pass_")]
     assert passes == ["pass_sketch", "pass_project"], passes
 
@@ -422,7 +411,7 @@ def test_autorank_ragged_and_power(rq, orc, b, l_max, q):
     g = rq.autorank(_cm(A), b=b, l_max=l_max, eps=5e-2, q=q, seed=8)
     o = orc.autorank(A, b=b, l_max=l_max, eps=5e-2, q=q, seed=8)
     assert g["l"] == o["l"]
-    _check_factorization(rq, orc, A, g, o, g["l"])
+    _check_factorization(rq, orc, A, g, o, g["l"], block=b)
 
 
 # ------------------------------------------------------------------ graph replay of the rare branches
@@ -446,9 +435,10 @@ def _wellcond(m, n, seed):
 
 @pytest.mark.parametrize("make,flag,d", [(_zero, 2, 0), (_deficient, 2, 2), (_illcond, 1, 0), (_wellcond, 0, 2)])
 def test_graph_replay_branches(rq, orc, make, flag, d):
-    """Each call with the same arguments runs eagerly first, then as a captured CUDA graph whose
-    rare orth branches (random completion, third CholeskyQR pass) are conditional nodes opened
-    on the device.  Eager and replayed results must be bitwise identical and flag the branch."""
+    """Each call with the same arguments runs eagerly first, then as a captured CUDA graph in which
+    the rare orth branch (the shifted CholeskyQR passes / random completion of orth_rescue.cu) is
+    an early-exiting cooperative kernel that decides on the device whether to work.  Eager and
+    replayed results must be bitwise identical and flag the branch."""
     A = make(400, 300, 5)
     h = rq.Handle()
     At = _cm(A)

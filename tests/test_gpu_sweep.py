@@ -2,10 +2,14 @@
 square, ragged against every tile size), k, p, q, d, b and spectra (polynomial, exponential,
 gapped, numerically rank-deficient, exactly rank-deficient) drawn from a fixed seed.  Every case
 checks the north_star tolerances where they are well defined and the basis-invariant quantities
-(residual, orthonormality) everywhere (readings R4, R26)."""
+(residual, orthonormality) everywhere (readings R4, R26).  The grading is tests/parity.py's:
+identical pivots (or a near-tie of the oracle's candidate norms, reading R30 -- anything else
+FAILS), L-values to max(1e-10 relative, C_L u |L_1|) (reading R29), Q, T, P element-wise, the
+residual to 1e-12 -- with a residual slack only for numerically rank-deficient sketches (R4)."""
 import numpy as np
 import pytest
 import torch
+from parity import check_factorization
 
 pytestmark = pytest.mark.gpu
 
@@ -62,37 +66,32 @@ def test_random_sweep(rq, orc, i):
     A, l = c["A"], c["k"] + c["p"]
     g = rq.factorize(_cm(A), c["k"], c["p"], q=c["q"], d=c["d"], b=c["b"], seed=c["seed"])
     if c["variant"] == "brqlp":
-        o = orc.brqlp(A, c["k"], c["p"], b=c["b"], q=c["q"], seed=c["seed"])
+        o = orc.brqlp(A, c["k"], c["p"], b=c["b"], q=c["q"], seed=c["seed"], stages=True)
+        B_o = o["V"].T @ A
     else:
-        o = orc.rqlp(A, c["k"], c["p"], q=c["q"], d=c["d"], seed=c["seed"])
+        o = orc.rqlp(A, c["k"], c["p"], q=c["q"], d=c["d"], seed=c["seed"], stages=True)
+        B_o = o["B"]
+        if c["d"] >= 1:
+            o["piv1"] = None
+    tag = f"case {i}: {c['variant']} m={c['m']} n={c['n']} k={c['k']} p={c['p']} q={c['q']} d={c['d']} b={c['b']} {c['kind']}"
+    _grade(orc, A, g, o, l, c["sig"], c["kind"], c["b"], B_o, tag)
+
+
+def _grade(orc, A, g, o, l, sig, kind, block, B_o, tag):
+    """Full grading where the factorisation is unique (a sketch of full numerical rank); the
+    basis-invariant quantities (residual with the R4 slack, orthonormality) otherwise."""
+    rank = int((sig > 1e-14 * sig[0]).sum())
+    if rank >= l and kind in ("poly", "exp", "gap"):
+        check_factorization(orc, A, g, o, l, sig_ratio=sig[:l] / sig[0], block=block, B_oracle=B_o, tag=tag)
+        return
     Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
     nA = np.linalg.norm(A)
     rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-    tag = f"case {i}: {c['variant']} m={c['m']} n={c['n']} k={c['k']} p={c['p']} q={c['q']} d={c['d']} b={c['b']} {c['kind']}"
-    # basis-invariant: orthonormal factors, the oracle's residual (to 1e-12, or relative to it when
-    # the sketch is numerically rank deficient and the completion directions differ)
-    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
-    if c["variant"] != "brqlp":   # BRQLP's P is orthonormal per block only (reading R17)
-        assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
+    lq = Q.shape[1]
+    assert np.abs(Q.T @ Q - np.eye(lq)).max() <= 1e-13 * lq, tag
+    if block is None:   # BRQLP's P is orthonormal per block only (reading R17)
+        assert np.abs(P.T @ P - np.eye(lq)).max() <= 1e-13 * lq, tag
     assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
-    # pivots and L-values where they are unique: full-rank sketch with separated leading values
-    rank = int((c["sig"] > 1e-14 * c["sig"][0]).sum())
-    if rank >= l and c["kind"] in ("poly", "exp", "gap"):
-        piv_g = g["piv0"].cpu().numpy()
-        if np.array_equal(piv_g, o["piv0"]):
-            # relative 1e-10 (north_star) where the L-value is above 1e-4 of the largest -- every
-            # L-value of C1-C5 (sigma_l/sigma_1 >= 2.9e-5); below that the achievable agreement
-            # of two FP64 computations is absolute, ~u ||A|| (gapped spectra reach 1e-7 relative)
-            Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
-            big = Lo >= 1e-4 * Lo.max()
-            rel = np.abs(Lg - Lo)[big] / Lo[big]
-            assert rel.max() <= 1e-10, (tag, rel.max())
-            assert np.abs(Lg - Lo).max() <= 1e-13 * Lo.max(), tag
-        else:
-            # a flip is possible only at a numerical near-tie of candidate norms;
-            # the residual already agreed above -- report the step instead of passing silently
-            first = int(np.argmax(piv_g != o["piv0"]))
-            pytest.xfail(f"{tag}: pivot sequences differ from step {first}")
 
 
 def _spectrum(rng, r, k, l):
@@ -130,20 +129,11 @@ def test_random_sweep_large(rq, orc, i):
     A = _rand_A(rng, m, n, sig)
     seed = int(rng.integers(0, 2**62))
     g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=seed)
-    o = orc.rqlp(A, k, p, q=q, d=d, seed=seed)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=seed, stages=True)
+    if d >= 1:
+        o["piv1"] = None
     tag = f"large {i}: m={m} n={n} k={k} p={p} q={q} d={d} {kind}"
-    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
-    nA = np.linalg.norm(A)
-    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
-    assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
-    assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
-    if kind != "numdef":
-        assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
-        Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
-        big = Lo >= 1e-4 * Lo.max()
-        assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
-        assert np.abs(Lg - Lo).max() <= 1e-13 * Lo.max(), tag
+    _grade(orc, A, g, o, l, sig, kind, None, o["B"], tag)
 
 
 @pytest.mark.parametrize("i", range(24))
@@ -165,27 +155,13 @@ def test_random_sweep_autorank_tqlp(rq, orc, i):
         o = orc.autorank(A, b, l_max, eps, q=q, seed=seed)
         tag = f"autorank {i}: m={m} n={n} b={b} l_max={l_max} eps={eps:.1e} q={q} {kind}"
         assert g["l"] == o["l"], (tag, g["l"], o["l"])
-        l = g["l"]
-        Q = _np(g["Q"])
-        assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * max(l, 1), tag
-        rg = orc.residual(A, Q, _np(g["T"]), _np(g["P"])) / nA
-        ro = orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-        assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
+        _grade(orc, A, g, o, g["l"], sig, kind, b, None, tag)
     else:
         l = int(rng.integers(2, min(m, n, 160) + 1))
         g = rq.tqlp(_cm(A), l)
         o = orc.tqlp(A, l)
         tag = f"tqlp {i}: m={m} n={n} l={l} {kind}"
-        Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
-        assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
-        assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
-        rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-        assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
-        if kind != "numdef":
-            assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
-            Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
-            big = Lo >= 1e-4 * Lo.max()
-            assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
+        _grade(orc, A, g, o, l, sig, kind, None, A, tag)
 
 
 def test_truncate_views(rq, orc):
@@ -230,17 +206,11 @@ def test_random_sweep_large_blocks(rq, orc, i):
         g = rq.autorank(_cm(A), b=b, l_max=l, eps=eps, q=q, seed=seed)
         o = orc.autorank(A, b, l, eps, q=q, seed=seed)
         assert g["l"] == o["l"], (tag, g["l"], o["l"])
-        lq = g["l"]
+        _grade(orc, A, g, o, g["l"], sig, kind, b, None, tag)
     else:
         g = rq.factorize(_cm(A), k, p, q=q, b=b, seed=seed)
-        o = orc.brqlp(A, k, p, b=b, q=q, seed=seed)
-        lq = l
-    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
-    assert np.abs(Q.T @ Q - np.eye(lq)).max() <= 1e-13 * lq, tag
-    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-    assert abs(rg - ro) <= 1e-12 or rg <= 2 * ro + 1e-14, (tag, rg, ro)
-    if kind != "numdef":
-        assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
+        o = orc.brqlp(A, k, p, b=b, q=q, seed=seed, stages=True)
+        _grade(orc, A, g, o, l, sig, kind, b, o["V"].T @ A, tag)
 
 
 _EDGE = [(l, sh, q, d) for l in (4, 32, 33, 128, 129, 257) for sh in ("square", "tall", "wide", "l_plus_1")
@@ -257,18 +227,11 @@ def test_edge_shapes(rq, orc, l, shape, q, d):
     A = _rand_A(rng, m, n, sig)
     k, p = l - 2, 2
     g = rq.factorize(_cm(A), k, p, q=q, d=d, seed=5)
-    o = orc.rqlp(A, k, p, q=q, d=d, seed=5)
-    Q, T, P = _np(g["Q"]), _np(g["T"]), _np(g["P"])
-    nA = np.linalg.norm(A)
+    o = orc.rqlp(A, k, p, q=q, d=d, seed=5, stages=True)
+    if d >= 1:
+        o["piv1"] = None
     tag = f"edge l={l} {shape} q={q} d={d}"
-    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13 * l, tag
-    assert np.abs(P.T @ P - np.eye(l)).max() <= 1e-13 * l, tag
-    rg, ro = orc.residual(A, Q, T, P) / nA, orc.residual(A, o["Q"], o["T"], o["P"]) / nA
-    assert abs(rg - ro) <= 1e-12, (tag, rg, ro)
-    assert np.array_equal(g["piv0"].cpu().numpy(), o["piv0"]), tag
-    Lg, Lo = np.abs(np.diag(T)), np.abs(np.diag(o["T"]))
-    big = Lo >= 1e-4 * Lo.max()
-    assert (np.abs(Lg - Lo)[big] / Lo[big]).max() <= 1e-10, tag
+    check_factorization(orc, A, g, o, l, sig_ratio=sig[:l] / sig[0], B_oracle=o["B"], tag=tag)
 
 
 def test_two_handles_on_two_streams_concurrently(rq):
