@@ -483,6 +483,7 @@ def main():
                 "roofline": roof, "roofline_whole_factorisation": whole, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(), "step_ms": [round(t, 4) for t in step_ms],
                 "stages_ms": {k: round(sum(v) / len(v), 4) for k, v in stage_ms.items()},
+                "stages_total_ms": {k: round(sum(v), 4) for k, v in stage_ms.items()},
                 "replicated_outputs_identical": replicated_identical, "device_flags": flags}
         print(json.dumps(line), flush=True)
     if group is not None:

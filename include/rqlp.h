@@ -171,7 +171,16 @@ int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, in
 int rqlp_factorize(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
                    const double *A, int64_t lda, uint64_t seed, double *Q, double *T, double *P, int *t_is_upper);
 
-/* Wait for the handle's stream; *flags (nullable) receives RQLP_FLAG_* bits of the last call. */
+/* The error indicator of eq. (3) (§6) of the last rqlp_ex /
+ * erqlp_ex / brqlp_ex / rqlp_autorank_ex / rqlp_factorize on h: *a2 = ||A||_F^2 (accumulated
+ * inside the first A-pass from the same A tiles, summed over the ranks of a sharded handle) and
+ * *b2 = ||B||_F^2 (BRQLP / auto-rank: sum_j ||B_j||_F^2 of the deflated B_j), so that
+ * ||A - V V^T A||_F^2 = *a2 - *b2 in exact arithmetic (V orthonormal).  Waits for the handle's
+ * stream.  Either pointer may be NULL. */
+int rqlp_get_indicator(rqlp_handle_t h, double *a2, double *b2);
+
+/* Wait for the handle's stream; *flags (nullable) receives RQLP_FLAG_* bits of the last call.
+ * On a NCCL handle an asynchronous NCCL failure (ncclCommGetAsyncError) returns RQLP_ERR_NCCL. */
 int rqlp_sync(rqlp_handle_t h, unsigned *flags);
 const char *rqlp_strerror(int code);
 

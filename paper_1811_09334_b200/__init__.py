@@ -149,6 +149,14 @@ class Handle:
         _check(lib().rqlp_sync(self.h, ctypes.byref(f)), "rqlp_sync")
         return f.value
 
+    def indicator(self) -> dict:
+        """eq. (3) of the last factorisation on this handle: ||A||_F^2, ||B||_F^2 (BRQLP: sum of the
+        deflated ||B_j||_F^2) and err = sqrt(max(0, a2 - b2)) / ||A||_F (PAPER.md:62-64)."""
+        a2, b2 = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        _check(lib().rqlp_get_indicator(self.h, ctypes.byref(a2), ctypes.byref(b2)), "rqlp_get_indicator")
+        a, b = a2.value, b2.value
+        return {"a2": a, "b2": b, "err": (max(0.0, a - b) ** 0.5 / a ** 0.5) if a > 0 else 0.0}
+
     def set_timing(self, on: bool):
         _check(lib().rqlp_set_timing(self.h, 1 if on else 0), "rqlp_set_timing")
 

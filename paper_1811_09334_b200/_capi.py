@@ -35,6 +35,7 @@ SIGNATURES = [
     ("rqlp_factorize", _int, [_vp, _int, _i64, _i64, _int, _int, _int, _int, _int, _vp, _i64, _u64, _vp, _vp, _vp,
                               ctypes.POINTER(_int)]),
     ("rqlp_sync", _int, [_vp, ctypes.POINTER(ctypes.c_uint)]),
+    ("rqlp_get_indicator", _int, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("rqlp_strerror", ctypes.c_char_p, [_int]),
     ("rqlp_omega", _int, [_vp, _i64, _i64, _u64, _vp, _i64]),
     ("rqlp_gemm_nn", _int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),

@@ -10,6 +10,14 @@
 
 #include <tuple>
 
+// Host-resident A of rqlp_factorize: copied in row panels on a copy stream while the sketch pass
+// consumes the panels that have landed (Y = AΩ is row-separable).
+struct HostFeed {
+  const double *hA = nullptr;
+  int64_t hlda = 0;
+  int64_t panel_rows = 0;
+};
+
 struct rqlp_handle_s {
   int magic = 0x51504c52;
   std::recursive_mutex mu;  // calls on one handle are serialised (the default handle is shared)
@@ -23,6 +31,7 @@ struct rqlp_handle_s {
   void *own = nullptr;  // library-owned (rqlp() / stage entry points without a workspace)
   size_t own_bytes = 0;
   unsigned *dflags = nullptr;
+  double *dind = nullptr;  // eq. (3) indicator terms of the last factorisation: ||A||_F^2, sum_j ||B_j||_F^2
   int64_t launches = 0;
   bool timing = false;
   std::vector<std::pair<std::string, cudaEvent_t>> events;
@@ -50,6 +59,9 @@ struct rqlp_handle_s {
   std::map<std::string, GEntry> graphs;
   std::map<std::string, int> seen;
   cudaStream_t gstream = nullptr;
+  const HostFeed *feed = nullptr;  // set by rqlp_factorize for its host A (one call at a time)
+  cudaStream_t cstream = nullptr;  // copy stream of the host feed and its events
+  std::vector<cudaEvent_t> cev;
   cudaStream_t side = nullptr;  // Ctx::branch() stream and its fork/join events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
@@ -97,6 +109,7 @@ Ctx make_ctx(rqlp_handle_t h) {
   c.device = h->device;
   c.num_sms = h->num_sms;
   c.dflags = h->dflags;
+  c.dind = h->dind;
   c.timing = h->timing;
   c.events = &h->events;
   c.pool = &h->eager_pool;
@@ -221,6 +234,11 @@ std::string make_key(rqlp_handle_t h, const char *tag, std::initializer_list<int
   put(&t, sizeof t);
   const void *st = (const void *)h->stream;
   put(&st, sizeof st);
+  if (h->feed) {   // host-fed A (rqlp_factorize): the copies are part of the captured work
+    put(&h->feed->hA, sizeof h->feed->hA);
+    put(&h->feed->hlda, sizeof h->feed->hlda);
+    put(&h->feed->panel_rows, sizeof h->feed->panel_rows);
+  }
   return k;
 }
 
@@ -229,6 +247,8 @@ struct Plan {
   int64_t m, n, l, ldm, ldn, ldl;
   double *Om, *Y, *V, *Z, *W, *B, *QB, *T, *PB, *part;
   size_t part_elems;
+  double *fro_slots;  // per-CTA partials of ||A||_F^2 (first A-pass) and of ||B||_F^2
+  int64_t fro_cap;
   OrthScratch orth;
   TailScratch tail;
   // BRQLP extras
@@ -250,6 +270,8 @@ void carve_plan(Arena &a, Plan &p, int variant, int64_t m, int64_t n, int64_t l,
   p.PB = a.take<double>(p.ldn * l);
   p.part_elems = std::max(gemm_partials_needed(m, l, n, num_sms), gemm_partials_needed(n, l, m, num_sms));
   p.part = a.take<double>((int64_t)p.part_elems);
+  p.fro_cap = fro_slots_cap(m, num_sms);
+  p.fro_slots = a.take<double>(p.fro_cap);
   orth_carve(a, p.orth, std::max(m, n), lb, num_sms);
   tail_carve(a, p.tail, lb, n, num_sms);
   if (variant == RQLP_VARIANT_BRQLP) {
@@ -345,6 +367,39 @@ int check_common(int64_t m, int64_t n, int k, int p, int q) {
   return 0;
 }
 
+// The sketch pass Y = A X (X = Ω or its first columns) with ||A||_F^2 fused.  With a host feed
+// the rows of A arrive in panels: panel p is copied on the copy stream and its rows of Y (and its
+// share of ||A||^2, accumulated in panel order) are computed as soon as it has landed.
+void sketch_pass(Ctx &c, rqlp_handle_t h, const Plan &P, int64_t m, int64_t cols, int64_t n, const double *A,
+                 int64_t lda, const double *X, int64_t ldx, double *Y, int64_t ldy) {
+  const HostFeed *f = h->feed;
+  if (!f) {
+    gemm_nn_fro(c, m, cols, n, A, lda, X, ldx, Y, ldy, P.part, P.part_elems, FroSpec{P.fro_slots, P.fro_cap, c.dind});
+    return;
+  }
+  const int64_t np = ceil_div(m, f->panel_rows);
+  if (!h->cstream) RQLP_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+  while ((int64_t)h->cev.size() < np + 1) {
+    cudaEvent_t e;
+    RQLP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->cev.push_back(e);
+  }
+  RQLP_CUDA(cudaEventRecord(h->cev[np], c.stream));          // fork: the copies follow earlier work
+  RQLP_CUDA(cudaStreamWaitEvent(h->cstream, h->cev[np], 0));
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t r0 = p * f->panel_rows, rows = std::min(f->panel_rows, m - r0);
+    RQLP_CUDA(cudaMemcpy2DAsync((void *)(A + r0), lda * 8, f->hA + r0, f->hlda * 8, rows * 8, n,
+                                cudaMemcpyHostToDevice, h->cstream));
+    RQLP_CUDA(cudaEventRecord(h->cev[p], h->cstream));
+  }
+  for (int64_t p = 0; p < np; ++p) {   // (the last wait also joins the copy stream)
+    const int64_t r0 = p * f->panel_rows, rows = std::min(f->panel_rows, m - r0);
+    RQLP_CUDA(cudaStreamWaitEvent(c.stream, h->cev[p], 0));
+    gemm_nn_fro(c, rows, cols, n, A + r0, lda, X, ldx, Y + r0, ldy, P.part, P.part_elems,
+                FroSpec{P.fro_slots, P.fro_cap, c.dind, p > 0});
+  }
+}
+
 // ---- RQLP / ERQLP ------------------------------------------------------------------------
 // Range finder + q subspace iterations (Alg.1 l.1-3 + reading R12), B = V^T A (Alg.1 l.4).
 void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, const double *A, int64_t lda,
@@ -353,7 +408,9 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   c.mark("start");
   launch_omega(c, n, l, 0, seed, P.Om, P.ldn);                                        // l.1
   c.mark("omega");
-  gemm_nn(c, m, l, n, A, lda, P.Om, P.ldn, P.Y, P.ldm, P.part, P.part_elems);         // l.2 Y = AΩ
+  // l.2 Y = AΩ, with ||A||_F^2 (eq. (3)) accumulated from the same A tiles
+  sketch_pass(c, h, P, m, l, n, A, lda, P.Om, P.ldn, P.Y, P.ldm);
+  allreduce_sum(c, c.dind, 1);   // row shards: ||A||^2 is the sum over ranks
   c.mark("pass_sketch");
   if (h->dbgY) launch_copy(c, m, l, P.Y, P.ldm, h->dbgY, h->ldY, false);
   // l.3 V = qr(Y); bases that only feed the next subspace-iteration product need just the span
@@ -377,6 +434,7 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.B, P.ldl, true, P.part, P.part_elems);    // l.4 B = V^T A
   allreduce_sum(c, P.B, P.ldl * n);
   c.mark("pass_project");
+  fro2_accumulate(c, l, n, P.B, P.ldl, P.fro_slots, c.dind + 1, true);   // ||B||_F^2 (replicated B)
   if (h->dbgV) launch_copy(c, m, l, P.V, P.ldm, h->dbgV, h->ldV, false);
   if (h->dbgB) launch_copy(c, l, n, P.B, P.ldl, h->dbgB, h->ldB, false);
 }
@@ -412,7 +470,6 @@ int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
 // it is <= (eps ||A||_F)^2 (reading R25).
 struct AutoRank {
   double eps = 0.0, a2 = 0.0, err = 0.0;
-  double *acc = nullptr, *part = nullptr;  // device: running sum_j ||B_j||^2, reduction partials
   int l_out = 0;
 };
 void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int b, int q, const double *A,
@@ -448,19 +505,13 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   c.mark("start");
   launch_omega(c, n, l, 0, seed, P.Om, ldn);                                            // l.1
   c.mark("omega");
+  const FroSpec fro{P.fro_slots, P.fro_cap, c.dind};
   if (!ar) {
-    gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);             // l.3 all Y_j = AΩ_j
+    // l.3 all Y_j = AΩ_j in one pass, with ||A||_F^2 (eq. (3)) from the same A tiles
+    sketch_pass(c, h, P, m, l, n, A, lda, P.Om, ldn, P.Y, ldm);
+    allreduce_sum(c, c.dind, 1);   // row shards: ||A||^2 is the sum over ranks (B_j is replicated)
     c.mark("pass_sketch");
     if (h->dbgY) launch_copy(c, m, l, P.Y, ldm, h->dbgY, h->ldY, false);
-  } else {
-    // ||A||_F^2 once (one read of A), then sum_j ||B_j||^2 accumulates on the device
-    fro2_accumulate(c, m, n, A, lda, ar->part, ar->acc, true);
-    allreduce_sum(c, ar->acc, 1);  // row shards: ||A||^2 is the sum over ranks (B_j is replicated)
-    double a2 = 0.0;
-    RQLP_CUDA(cudaMemcpyAsync(&a2, ar->acc, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    RQLP_CUDA(cudaStreamSynchronize(c.stream));
-    ar->a2 = a2;
-    RQLP_CUDA(cudaMemsetAsync(ar->acc, 0, sizeof(double), c.stream));
   }
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
@@ -502,9 +553,14 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   for (int64_t j = 0; j < h_blocks; ++j) {
     const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
     double *Vj = P.V + c0 * ldm;
-    if (ar) {  // Alg.3 l.3 inside the loop: Y_j = A Ω_j (original A)
+    if (ar) {  // Alg.3 l.3 inside the loop: Y_j = A Ω_j (original A); the first pass also forms ||A||_F^2
       c.mark("b_other");
-      gemm_nn(c, m, bj, n, A, lda, P.Om + c0 * ldn, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems);
+      if (j == 0) {
+        gemm_nn_fro(c, m, bj, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems, fro);
+        allreduce_sum(c, c.dind, 1);
+      } else {
+        gemm_nn(c, m, bj, n, A, lda, P.Om + c0 * ldn, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems);
+      }
       c.mark("pass_block_sketch");
     }
     if (!two_pass) {
@@ -561,10 +617,12 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     c.mark("block_passes");
     bool stop = false;
     if (ar) {  // eq. (3): ||A - P_V A||_F^2 = ||A||_F^2 - sum_j ||B_j||_F^2
-      fro2_accumulate(c, bj, n, Bj, ldbj, ar->part, ar->acc, false);
-      double b2 = 0.0;
-      RQLP_CUDA(cudaMemcpyAsync(&b2, ar->acc, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+      fro2_accumulate(c, bj, n, Bj, ldbj, P.fro_slots, c.dind + 1, j == 0);
+      double ab[2] = {0.0, 0.0};
+      RQLP_CUDA(cudaMemcpyAsync(ab, c.dind, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
       RQLP_CUDA(cudaStreamSynchronize(c.stream));
+      ar->a2 = ab[0];
+      const double b2 = ab[1];
       const double e2 = ar->a2 - b2;
       ar->err = ar->a2 > 0.0 ? std::sqrt(e2 > 0.0 ? e2 : 0.0) / std::sqrt(ar->a2) : 0.0;
       ar->l_out = (int)(c0 + bj);
@@ -578,6 +636,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     c.mark("block_tail");
     if (stop) break;
   }
+  if (!ar) fro2_accumulate(c, l, n, B, LL, P.fro_slots, c.dind + 1, true);   // sum_j ||B_j||_F^2 (deflated B_j)
   if (h->dbgV) launch_copy(c, m, l, P.V, ldm, h->dbgV, h->ldV, false);
   if (h->dbgB) launch_copy(c, l, n, B, LL, h->dbgB, h->ldB, false);
 }
@@ -650,6 +709,8 @@ int rqlp_create(rqlp_handle_t *out, int device, void *cuda_stream) {
   cudaSetDevice(device);
   cudaError_t e = cudaMalloc(&h->dflags, NUM_DEV_FLAGS * sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(h->dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMalloc(&h->dind, 4 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(h->dind, 0, 4 * sizeof(double));
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     delete h;
@@ -730,11 +791,14 @@ int rqlp_destroy(rqlp_handle_t h) {
   for (auto ev : h->eager_pool) cudaEventDestroy(ev);
   if (h->gstream) cudaStreamDestroy(h->gstream);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
+  for (auto ev : h->cev) cudaEventDestroy(ev);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own) cudaFree(h->own);
   if (h->stage) cudaFree(h->stage);
   if (h->dflags) cudaFree(h->dflags);
+  if (h->dind) cudaFree(h->dind);
   comm_destroy(h->comm);
   cudaSetDevice(prev);
   h->magic = 0;
@@ -869,11 +933,9 @@ int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, in
   if (!l_out) return -19;
   return guarded(h, [&] {
     const size_t need = plan_bytes(RQLP_VARIANT_BRQLP, m, n, l_max, b, h->num_sms);
-    char *ws = get_ws(h, need + 1032 * 8 + 256, true);
+    char *ws = get_ws(h, need, true);
     AutoRank ar;
     ar.eps = eps;
-    ar.acc = reinterpret_cast<double *>(ws + ((need + 255) & ~(size_t)255));
-    ar.part = ar.acc + 8;
     Ctx c = make_ctx(h);
     reset_timing(h);
     // k + p = l_max for the plan; the loop stops at the first block meeting the tolerance
@@ -895,6 +957,15 @@ static bool is_device_ptr(const void *p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+static bool is_pinned_host_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 static std::mutex g_default_mu;
 static rqlp_handle_t g_default[64] = {nullptr};
 
@@ -905,8 +976,8 @@ static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int
   int64_t l = (int64_t)k + p;
   return guarded(h, [&] {
     bool dA = is_device_ptr(A), dQ = is_device_ptr(Q), dT = is_device_ptr(T), dP = is_device_ptr(P);
-    size_t nA = (size_t)(lda * (n - 1) + m);
-    size_t szA = dA ? 0 : (size_t)round_up((int64_t)nA, 32) * 8;
+    const int64_t ldd = dA ? lda : round_up(m, 8);   // device staging of a host A: aligned for TMA
+    size_t szA = dA ? 0 : (size_t)round_up(ldd * n, 32) * 8;
     size_t szQ = dQ ? 0 : (size_t)round_up(m * l, 32) * 8;
     size_t szT = dT ? 0 : (size_t)round_up(l * l, 32) * 8;
     size_t szP = dP ? 0 : (size_t)round_up(n * l, 32) * 8;
@@ -925,13 +996,30 @@ static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int
     if (!dQ) { Qd = (double *)sp; sp += szQ; }
     if (!dT) { Td = (double *)sp; sp += szT; }
     if (!dP) { Pd = (double *)sp; sp += szP; }
-    if (!dA) RQLP_CUDA(cudaMemcpyAsync((void *)Ad, A, nA * 8, cudaMemcpyHostToDevice, h->stream));
+    // host A: copied in row panels inside the factorisation, overlapped with the sketch pass that
+    // consumes them (sketch_pass); the panel height keeps each copy >= ~0.5 GB and <= 8 panels
+    HostFeed feed;
+    if (!dA && !is_pinned_host_ptr(A)) {   // pageable: one synchronous-source copy up front
+      RQLP_CUDA(cudaMemcpy2DAsync((void *)Ad, ldd * 8, A, lda * 8, m * 8, n, cudaMemcpyHostToDevice, h->stream));
+    } else if (!dA) {
+      feed.hA = A;
+      feed.hlda = lda;
+      const int64_t min_rows = std::max<int64_t>(128, ceil_div((int64_t)1 << 26, n));
+      feed.panel_rows = round_up(std::max(min_rows, ceil_div(m, 8)), 128);
+      h->feed = &feed;
+    }
     int r;
-    if (variant == RQLP_VARIANT_BRQLP)
-      r = run_brqlp(h, m, n, k, p, b, q, Ad, lda, seed, Qd, m, Td, l, Pd, n, nullptr, nullptr, true);
-    else
-      r = run_rqlp(h, m, n, k, p, q, variant == RQLP_VARIANT_ERQLP ? d : 0, Ad, lda, seed, Qd, m, Td, l, Pd, n,
-                   nullptr, nullptr, true);
+    try {
+      if (variant == RQLP_VARIANT_BRQLP)
+        r = run_brqlp(h, m, n, k, p, b, q, Ad, ldd, seed, Qd, m, Td, l, Pd, n, nullptr, nullptr, true);
+      else
+        r = run_rqlp(h, m, n, k, p, q, variant == RQLP_VARIANT_ERQLP ? d : 0, Ad, ldd, seed, Qd, m, Td, l, Pd, n,
+                     nullptr, nullptr, true);
+    } catch (...) {
+      h->feed = nullptr;
+      throw;
+    }
+    h->feed = nullptr;
     if (r) return r;
     if (t_is_upper) *t_is_upper = (variant == RQLP_VARIANT_ERQLP && d % 2 == 0) ? 1 : 0;
     if (!dQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -996,6 +1084,17 @@ int rqlp_sync(rqlp_handle_t h, unsigned *flags) {
       RQLP_CUDA(cudaMemcpy(&f, h->dflags + FLAG_WORD, sizeof(unsigned), cudaMemcpyDeviceToHost));
       *flags = f;
     }
+    return RQLP_OK;
+  });
+}
+
+int rqlp_get_indicator(rqlp_handle_t h, double *a2, double *b2) {
+  return guarded(h, [&] {
+    double v[2] = {0.0, 0.0};
+    RQLP_CUDA(cudaStreamSynchronize(h->stream));
+    RQLP_CUDA(cudaMemcpy(v, h->dind, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (a2) *a2 = v[0];
+    if (b2) *b2 = v[1];
     return RQLP_OK;
   });
 }

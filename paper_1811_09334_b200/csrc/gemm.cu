@@ -212,7 +212,7 @@ void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
 // ---- tall-skinny passes ------------------------------------------------------------------
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
                  int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask, int tri);
+                 unsigned cond_mask, int tri, const FroSpec *fro = nullptr);
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
                  int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
                  const unsigned *cond, unsigned cond_mask, int tri);
@@ -231,6 +231,13 @@ void gemm_nn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t 
   if (gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri)) return;
   gemm_generic_ex(c, false, false, m, cc, k, 1.0, A, lda, X, ldx, 0.0, Y, ldy, partials, partial_elems, false, cond,
                   cond_mask);
+}
+
+void gemm_nn_fro(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+                 int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const FroSpec &fro) {
+  if (gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, nullptr, 0, 0, &fro)) return;
+  gemm_nn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems);
+  fro2_accumulate(c, m, k, A, lda, fro.slots, fro.out, !fro.accumulate);
 }
 
 void gemm_tn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,

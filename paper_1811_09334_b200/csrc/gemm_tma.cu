@@ -73,12 +73,12 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 
 // MODE 0 = NN, 1 = TN.  Output element (i, j) of the (M x N) product goes to
 //   part (split-K slice, M x N contiguous)  or  C[i + j ldc]  or (trans) C[j + i ldc].
-template <int BN, int MODE>
+template <int BN, int MODE, bool FRO>
 __global__ void __launch_bounds__(NCONS * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
                     double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri, int bal_units,
-                    int ntn, int maxc) {
+                    int ntn, int maxc, double *__restrict__ fro_slots) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   // tri == 1: only the upper triangle of the (symmetric) output is wanted -- tiles strictly below
   // the diagonal do nothing (a Gram; consumers read the upper triangle).  tri == 2: the B operand
@@ -161,8 +161,17 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): the warps of column
+  // half wn = 0 hold every A element of the k-tile exactly once in their fragments; only the CTAs
+  // of output column tile 0 count (the other column tiles re-read A).  A compile-time switch: a
+  // runtime one cost the plain NN kernel ~10 % (32 more registers, a branch in the MMA loop).
+  static_assert(!FRO || MODE == 0, "||A||^2 is fused into the NN pass only");
+  double fro = 0.0;
+  const bool fro_on = FRO && wn == 0 && (bal || n0 == 0);
   for (int it = 0; it < nkt; ++it) {
     const int s = it % STAGES;
+    // balanced runs: the unit's tile is in output column tile 0
+    const bool fro_it = fro_on && (!bal || ((u0 + it) / ktiles_total) % ntn == 0);
     if (threadIdx.x == 0 && it + STAGES - 1 < nkt) {
       // refill the slot consumed at iteration it-1 once every warp has released it
       if (it >= 1) mbar_wait(&empty[(it - 1) % STAGES], ((it - 1) / STAGES) & 1);
@@ -180,6 +189,10 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
         if (MODE == 0) {
           a0[mb] = sa[(kk * 8 + 2 * cq) * LDA_NN + row];
           a1[mb] = sa[(kk * 8 + 2 * cq + 1) * LDA_NN + row];
+          if (fro_it) {
+            fro = fma(a0[mb], a0[mb], fro);
+            fro = fma(a1[mb], a1[mb], fro);
+          }
         } else {
           const double2 v = *reinterpret_cast<const double2 *>(sa + row * BK + kk * 8 + 2 * cq);
           a0[mb] = v.x;
@@ -215,6 +228,19 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
           acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
         }
       }
+    }
+  }
+  if (FRO) {   // per-CTA partial of ||A||_F^2, fixed-order reduction
+    __shared__ double fro_red[NCONS];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+    if (lane == 0) fro_red[warp] = fro;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < NCONS; ++w) t += fro_red[w];
+      fro_slots[blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)] = t;
     }
   }
   if (bal) return;
@@ -302,6 +328,21 @@ __global__ void __launch_bounds__(256) bal_reduce_kernel(int M, int N, int bn, i
   }
 }
 
+// *out = sum of the n fro slots: thread t sums slots t, t + 256, ... in order, then a fixed tree.
+__global__ void __launch_bounds__(256) fro_reduce_kernel(const double *__restrict__ slots, int n, double *out,
+                                                         int accumulate) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) s += slots[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = accumulate ? *out + red[0] : red[0];
+}
+
 // ------------------------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -364,6 +405,48 @@ int choose_bn_mk(int64_t M, int64_t c, int64_t ktiles, int num_sms) {
   return best;
 }
 
+// Output columns covered by tiles of two widths when one width leaves padding: the first c1 = t1 bn1
+// columns in one launch, the remaining cc - c1 in a second launch with one tile of width bn2 >= the
+// remainder (e.g. l = 528 -> 4 x 112 + 80 instead of 5 x 112 = 560; l = 272 -> 144 + 128 instead of
+// 2 x 144).  Only for long-K passes (the A-passes), where the padded columns cost their full DMMA
+// work; returns c1 = 0 when one width is as good.
+struct ColSplit {
+  int64_t c1 = 0;
+  int bn1 = 0, bn2 = 0;
+};
+bool env_off(const char *name) {
+  const char *e = getenv(name);
+  return e && e[0] == '0';
+}
+
+ColSplit choose_colsplit(int64_t cc, int64_t ktiles) {
+  ColSplit best;
+  static const bool off = env_off("RQLP_GEMM_COLSPLIT");   // measurement switch
+  if (off || ktiles <= 16 || cc <= 64) return best;
+  const int bn = choose_bn(cc);
+  const int64_t pad1 = ceil_div(cc, bn) * bn - cc;
+  if (pad1 * 50 < cc) return best;   // < 2 % padding: not worth a second launch
+  int64_t best_pad = pad1;
+  for (int b1 : kBNs) {
+    if (b1 < 64) continue;
+    const int64_t t1 = cc / b1;
+    const int64_t c1 = t1 * b1, rem = cc - c1;
+    if (t1 < 1 || rem <= 0) continue;
+    for (int b2 : kBNs) {
+      if (b2 < rem || (b2 < 64 && rem > 64)) continue;
+      const int64_t pad = b2 - rem;
+      if (pad < best_pad || (pad == best_pad && best.c1 > 0 && b1 > best.bn1)) {
+        best_pad = pad;
+        best.c1 = c1;
+        best.bn1 = b1;
+        best.bn2 = b2;
+      }
+      break;   // the smallest b2 covering the remainder
+    }
+  }
+  return best;
+}
+
 // Split-K: minimise the modelled time  waves(T) * ceil(ktiles / S) * t_ktile
 //                                      + (S > 1) * (2 S M N 8 bytes / HBM + reduce launch)
 // with T = tiles * S CTAs (1 CTA per SM), t_ktile = 128 BN 24 2 flop / (DMMA peak per SM).
@@ -413,19 +496,28 @@ BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t parti
   return p;
 }
 
-template <int BN, int MODE>
-void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp) {
+template <int BN, int MODE, bool FRO>
+void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+                 int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
+                 const FroSpec *fro) {
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
-  smem_attr((const void *)gemm_tma_kernel<BN, MODE>, SMEM);
+  smem_attr((const void *)gemm_tma_kernel<BN, MODE, FRO>, SMEM);
+  double *fslots = fro ? fro->slots : nullptr;
+  auto fro_finish = [&](int64_t nctas) {
+    if (!fro) return;
+    fro_reduce_kernel<<<1, 256, 0, c.stream>>>(fro->slots, (int)nctas, fro->out, fro->accumulate ? 1 : 0);
+    RQLP_LAUNCHED(c);
+  };
   if (bp.units > 0) {
     const int ntn = (int)ceil_div(N, BN);
     const int64_t total = (int64_t)ktiles * ntn * ceil_div(M, BM);
     const unsigned ctas = (unsigned)ceil_div(total, bp.units);
-    gemm_tma_kernel<BN, MODE><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
-                                                                     part, cond, mask, 0, bp.units, ntn, bp.maxc);
+    gemm_tma_kernel<BN, MODE, FRO><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
+                                                                     part, cond, mask, 0, bp.units, ntn, bp.maxc,
+                                                                     fslots);
     RQLP_LAUNCHED(c);
+    fro_finish(ctas);
     const int grid = (int)std::min<int64_t>(ceil_div(M, 32) * ceil_div(N, 32), (int64_t)c.num_sms * 8);
     bal_reduce_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(M, N, BN, ntn, ktiles, bp.units, bp.maxc, part, C, ldc,
                                                                 trans ? 1 : 0, cond, mask);
@@ -435,26 +527,41 @@ void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int 
   int kps = (int)ceil_div(ktiles, S);
   S = (int)ceil_div(ktiles, kps);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
-  gemm_tma_kernel<BN, MODE><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
+  gemm_tma_kernel<BN, MODE, FRO><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
-                                                                       mask, tri, 0, 1, 1);
+                                                                       mask, tri, 0, 1, 1, fslots);
   RQLP_LAUNCHED(c);
+  fro_finish((int64_t)grid.x * grid.y * grid.z);
   if (S > 1) launch_reduce(c, M, N, S, part, 1.0, 0.0, C, ldc, trans, cond, mask);
+}
+
+template <int BN, int MODE>
+void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
+               const FroSpec *fro) {
+  if constexpr (MODE == 0) {
+    if (fro) {
+      launch_bn_t<BN, 0, true>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro);
+      return;
+    }
+  }
+  launch_bn_t<BN, MODE, false>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, nullptr);
 }
 
 template <int MODE>
 void dispatch(Ctx &c, int bn, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
-              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp) {
+              int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
+              const FroSpec *fro = nullptr) {
   switch (bn) {
-    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
-    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp); break;
+    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
   }
 }
 
@@ -479,27 +586,59 @@ bool tma_disabled() {
 }  // namespace
 
 size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
-  // upper bound over both modes for the shapes (m, cc, k) and (k, cc, m)
+  // upper bound over both modes for the shapes (m, cc, k) and (k, cc, m), including the two
+  // launches of a two-width column split
   size_t best = 0;
+  auto need = [&](int64_t M, int64_t cols, int64_t ktiles, int bn) {
+    int64_t tiles = ceil_div(M, BM) * ceil_div(cols, bn);
+    double ts = 0.0;
+    int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cols, bn, &ts);
+    if (S > 1) best = std::max(best, (size_t)S * M * cols);
+    BalPlan bp = choose_balanced(tiles, ktiles, num_sms, (size_t)1 << 62, bn, ts);
+    if (bp.units > 0) best = std::max(best, (size_t)tiles * bp.maxc * BM * bn);
+  };
   for (int mode = 0; mode < 2; ++mode) {
     int64_t M = mode == 0 ? m : k, K = mode == 0 ? k : m;
     int64_t ktiles = ceil_div(K, BK);
-    int bn = choose_bn_mk(M, cc, ktiles, num_sms);
-    int64_t tiles = ceil_div(M, BM) * ceil_div(cc, bn);
-    double ts = 0.0;
-    int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cc, bn, &ts);
-    if (S > 1) best = std::max(best, (size_t)S * M * cc);
-    BalPlan bp = choose_balanced(tiles, ktiles, num_sms, (size_t)1 << 62, bn, ts);
-    if (bp.units > 0) best = std::max(best, (size_t)tiles * bp.maxc * BM * bn);
+    need(M, cc, ktiles, choose_bn_mk(M, cc, ktiles, num_sms));
+    const ColSplit cs = choose_colsplit(cc, ktiles);
+    if (cs.c1 > 0) {
+      need(M, cs.c1, ktiles, cs.bn1);
+      need(M, cc - cs.c1, ktiles, cs.bn2);
+    }
   }
   return best;
 }
 
+bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+                    int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
+                    unsigned cond_mask, int tri, const FroSpec *fro, int bn);
+
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X, int64_t ldx,
                  double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask, int tri) {
+                 unsigned cond_mask, int tri, const FroSpec *fro) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
-  int bn = choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms);
+  static const bool fro_off = env_off("RQLP_FRO_FUSED");   // measurement switch: separate ||A||^2 pass
+  if (fro && (cond || tri || fro_off)) return false;
+  const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(k, BK)) : ColSplit();
+  if (cs.c1 > 0) {
+    CUtensorMap probe;   // both column ranges must be TMA-addressable, else one width
+    if (make_map(&probe, X + cs.c1 * ldx, k, cc - cs.c1, ldx, BK, cs.bn2) &&
+        gemm_nn_tma_bn(c, m, cs.c1, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, 0, fro,
+                       cs.bn1)) {
+      if (!gemm_nn_tma_bn(c, m, cc - cs.c1, k, A, lda, X + cs.c1 * ldx, ldx, Y + cs.c1 * ldy, ldy, partials,
+                          partial_elems, cond, cond_mask, 0, nullptr, cs.bn2))
+        throw CudaError("gemm_nn_tma: second column range not launchable");
+      return true;
+    }
+  }
+  return gemm_nn_tma_bn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri, fro,
+                        choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms));
+}
+
+bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+                    int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
+                    unsigned cond_mask, int tri, const FroSpec *fro, int bn) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, m, k, lda, LDA_NN, BK)) return false;
   if (!make_map(&mb, X, k, cc, ldx, BK, bn)) return false;
@@ -510,15 +649,43 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   BalPlan bp;
   if (tri == 0 && partials && !balanced_disabled())
     bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
-  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri, bp);
+  if (fro) {   // the slots needed by this launch configuration must fit
+    const int64_t ctas = bp.units > 0 ? ceil_div(tiles * ktiles, bp.units)
+                                      : tiles * ceil_div(ktiles, ceil_div(ktiles, S));
+    if (ctas > fro->cap) return false;
+  }
+  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri, bp, fro);
   return true;
 }
+
+bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
+                    int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
+                    const unsigned *cond, unsigned cond_mask, int tri, int bn);
 
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
                  double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
                  unsigned cond_mask, int tri) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
-  int bn = choose_bn_mk(k, cc, ceil_div(m, BK), c.num_sms);
+  const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(m, BK)) : ColSplit();
+  if (cs.c1 > 0) {
+    CUtensorMap probe;
+    double *Z2 = trans_out ? Z + cs.c1 : Z + cs.c1 * ldz;
+    if (make_map(&probe, V + cs.c1 * ldv, m, cc - cs.c1, ldv, BK, cs.bn2) &&
+        gemm_tn_tma_bn(c, m, cs.c1, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask, 0,
+                       cs.bn1)) {
+      if (!gemm_tn_tma_bn(c, m, cc - cs.c1, k, A, lda, V + cs.c1 * ldv, ldv, Z2, ldz, trans_out, partials,
+                          partial_elems, cond, cond_mask, 0, cs.bn2))
+        throw CudaError("gemm_tn_tma: second column range not launchable");
+      return true;
+    }
+  }
+  return gemm_tn_tma_bn(c, m, cc, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask, tri,
+                        choose_bn_mk(k, cc, ceil_div(m, BK), c.num_sms));
+}
+
+bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
+                    int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
+                    const unsigned *cond, unsigned cond_mask, int tri, int bn) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, m, k, lda, BK, BM)) return false;
   if (!make_map(&mb, V, m, cc, ldv, BK, bn)) return false;

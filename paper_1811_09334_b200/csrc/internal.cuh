@@ -108,6 +108,7 @@ struct Ctx {
   int num_sms = 148;
   int64_t launches = 0;
   unsigned *dflags = nullptr;     // NUM_DEV_FLAGS words of device memory
+  double *dind = nullptr;         // ||A||_F^2, sum_j ||B_j||_F^2 of the current factorisation
   bool timing = false;
   std::vector<std::pair<std::string, cudaEvent_t>> *events = nullptr;
   std::vector<cudaEvent_t> *pool = nullptr;  // pre-created events (no cudaEventCreate under capture)
@@ -174,6 +175,19 @@ struct Arena {
 void launch_omega(Ctx &c, int64_t n, int64_t l, int64_t col0, uint64_t seed, double *Om, int64_t ldo);
 
 // ---- GEMM (gemm.cu) ----
+// ||A||_F^2 fused into an NN pass over A: per-CTA partials in `slots` (capacity `cap`), summed in
+// fixed order into *out (device double).
+struct FroSpec {
+  double *slots = nullptr;
+  int64_t cap = 0;
+  double *out = nullptr;
+  bool accumulate = false;  // *out += (row panels of one A), else *out =
+};
+static inline int64_t fro_slots_cap(int64_t m, int num_sms) { return ceil_div(m, 128) * 8 + 8 * (int64_t)num_sms; }
+// Y = A X and *fro->out = ||A||_F^2 (the first A-pass; a separate fixed-order pass over A when the
+// fused TMA kernel cannot be used)
+void gemm_nn_fro(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
+                 int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const FroSpec &fro);
 // C = alpha op(A) op(B) + beta C (generic DMMA kernel; any layout / alignment).
 void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
                   int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,

@@ -12,9 +12,9 @@ north_star's literal numbers).
     the achievable agreement of two FP64 computations is absolute (reading R29);
   * |‖A−QTPᵀ‖_F − ‖A−Q_oT_oP_oᵀ‖_F| / ‖A‖_F <= 1e-12;  ‖QᵀQ − I‖_max <= 1e-13 l;
     ‖PᵀP − I‖_max <= 1e-13 l (per block for BRQLP, reading R17);
-  * element-wise (Q, T, P are unique given the pivots, reading R3): column j of Q and P within
-    C_QP u |L_1|/|L_j|, T within C_T u |L_1| (perturbation of the j-th pivoted-QR direction
-    ~ u ‖B‖ / |R_jj|).
+  * element-wise (Q, T, P are unique given the pivots, reading R3): column j of Q within
+    C_Q u |L_1|/|L_j|, of P within C_P u |L_1|/|L_j|, T within C_T u |L_1| (perturbation of the
+    j-th pivoted-QR direction ~ u ‖B‖ / |R_jj|).
 
 RQLP_PARITY_LOG=<file> appends one JSON record per comparison with the normalised errors (the
 calibration data of DESIGN.md §6).
@@ -27,10 +27,13 @@ import os
 import numpy as np
 
 U = 2.0 ** -53
+# Constants calibrated on the whole -m gpu suite (RQLP_PARITY_LOG): largest measured
+# normalised errors 38 (L), 1830 (Q), 14 (P), 38 (T); each bound leaves a margin of >= 1.7x.
 TIE_REL = 1e-8       # R30: downdated-norm agreement of two FP64 CPQRs (LAPACK recompute at sqrt(u))
-C_L = 2048.0         # R29: |ΔL_j| floor in units of u |L_1|
-C_QP = 2.0 ** 16     # column j of Q, P: C_QP u |L_1| / |L_j|
-C_T = 2.0 ** 12      # T entries: C_T u |L_1|
+C_L = 64.0           # R29: |ΔL_j| floor in units of u |L_1|
+C_Q = 4096.0         # column j of Q: C_Q u |L_1| / |L_j|
+C_P = 256.0          # column j of P: C_P u |L_1| / |L_j|
+C_T = 128.0          # T entries: C_T u |L_1|
 
 
 def _np(t):
@@ -142,8 +145,8 @@ def check_factorization(orc, A, g, o, l, sig_ratio=None, block=None, B_oracle=No
         dT = np.abs(T[:jmax, :jmax] - o["T"][:jmax, :jmax]).max()
         rec["T_over"] = float(dT / (U * L1))
         if not os.environ.get("RQLP_PARITY_CALIBRATE"):
-            assert rec["Q_over"] <= C_QP, (tag, "Q elementwise", rec)
-            assert rec["P_over"] <= C_QP, (tag, "P elementwise", rec)
+            assert rec["Q_over"] <= C_Q, (tag, "Q elementwise", rec)
+            assert rec["P_over"] <= C_P, (tag, "P elementwise", rec)
             assert rec["T_over"] <= C_T, (tag, "T elementwise", rec)
     _log(rec)
     return rec

@@ -489,3 +489,41 @@ def test_extreme_scale_terminates(rq, orc, scale):
     Q = _np(g["Q"])
     ok = np.isfinite(Q).all() and np.abs(Q.T @ Q - np.eye(14)).max() <= 1e-12
     print(f"scale {scale:g}: flags {flags}, Q finite and orthonormal: {ok}")
+
+
+# ------------------------------------------------------------------ eq. (3) indicator (§8 a10)
+IND_CASES = [  # (name, m, n, k, p, q, d, b, col-major padding of A)
+    ("rqlp", 1000, 800, 20, 5, 0, 0, None, 0),
+    ("erqlp", 1031, 1030, 100, 10, 1, 2, None, 0),
+    ("brqlp", 1500, 700, 120, 16, 1, 0, 64, 0),
+    ("brqlp_q0", 1200, 500, 60, 12, 0, 0, 16, 0),
+    ("odd_lda_fallback", 700, 500, 40, 8, 1, 2, None, 1),   # lda odd: no TMA map, separate fro pass
+]
+
+
+@pytest.mark.parametrize("case", IND_CASES, ids=[c[0] for c in IND_CASES])
+def test_indicator_eq3(rq, orc, case):
+    """||A||_F^2 accumulated inside the first A-pass and ||B||_F^2 (BRQLP: the deflated B_j) give
+    the eq. (3) identity ||A - V V^T A||_F^2 = ||A||^2 - ||B||^2: each term
+    against the oracle, the difference against the oracle's and against the direct residual."""
+    name, m, n, k, p, q, d, b, pad = case
+    sig = np.exp(-np.arange(1, min(m, n) + 1.0) / 40)
+    A = _rand_svd(m, n, sig, m + 7 * n)
+    Ad = torch.zeros(n, m + pad, dtype=torch.float64, device="cuda")
+    Ad[:, :m] = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    Ad = Ad.t()[:m]                                  # column-major view, lda = m + pad
+    h = rq.Handle()
+    g = rq.factorize(Ad, k, p, q=q, d=d, b=b, seed=13, handle=h)
+    ind = h.indicator()
+    a2_o = orc.fro(A) ** 2
+    if b is None:
+        o = orc.rqlp(A, k, p, q=q, d=d, seed=13, stages=True)
+        b2_o = orc.fro(o["B"]) ** 2
+    else:
+        o = orc.brqlp(A, k, p, b=b, q=q, seed=13, stages=True)
+        b2_o = orc.fro(orc.gemm_tn(o["V"], A)) ** 2   # sum_j ||B_j||^2 = ||V^T A||^2 (V orthonormal)
+    assert ind["a2"] == pytest.approx(a2_o, rel=1e-13)
+    assert ind["b2"] == pytest.approx(b2_o, rel=1e-12)
+    assert abs((ind["a2"] - ind["b2"]) - (a2_o - b2_o)) <= 1e-12 * a2_o
+    res = orc.residual(A, _np(g["Q"]), _np(g["T"]), _np(g["P"]))
+    assert abs((ind["a2"] - ind["b2"]) - res ** 2) <= 1e-12 * a2_o
