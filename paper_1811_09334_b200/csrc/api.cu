@@ -529,8 +529,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     for (int pass = 0; pass < 2; ++pass) {
       gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
       allreduce_sum(c, P.C, LL * bj);
-      gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems, false,
-                      nullptr, 0);
+      gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems);   // Vj -= V_<j C
       launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
       orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
     }
@@ -575,8 +574,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
         if (c0 > 0) {
           gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems); // C = V_<j^T Vj
           allreduce_sum(c, P.C, LL * bj);
-          gemm_generic_ex(c, true, false, n, bj, c0, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems, false,
-                          nullptr, 0);                                                     // Z -= B_<j^T C
+          gemm_tn_ab(c, c0, bj, n, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems);   // Z -= B_<j^T C
         }
         if (h->dbgZ) launch_copy(c, n, bj, P.Z, ldn, h->dbgZ + (it * l + c0) * h->ldZ, h->ldZ, false);
         orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
@@ -585,10 +583,8 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
         gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
         c.mark("pass_block_AW");
         if (c0 > 0) {
-          gemm_generic_ex(c, false, false, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems, false,
-                          nullptr, 0);                                                     // D = B_<j W
-          gemm_generic_ex(c, false, false, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part,
-                          P.part_elems, false, nullptr, 0);                                // Y -= V_<j D
+          gemm_nn_ab(c, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems);    // D = B_<j W
+          gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part, P.part_elems);  // Y -= V_<j D
         }
         if (h->dbgYP) launch_copy(c, m, bj, P.Y + c0 * ldm, ldm, h->dbgYP + (it * l + c0) * h->ldYP, h->ldYP, false);
         orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
@@ -610,8 +606,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       const int64_t lde = round_up(b, 8);
       gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, lde, false, P.part, P.part_elems);   // E = Vj^T V_<j (bj x c0)
       allreduce_sum(c, P.D, lde * c0);
-      gemm_generic_ex(c, false, false, bj, n, c0, -1.0, P.D, lde, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems, false,
-                      nullptr, 0);
+      gemm_nn_ab(c, bj, n, c0, -1.0, P.D, lde, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems);   // B_j -= E B_<j
     }
     launch_copy(c, bj, n, Bj, ldbj, B + c0, LL, false);   // keep B_j for the later blocks' deflation
     c.mark("block_passes");

@@ -212,10 +212,10 @@ void gemm_generic(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
 // ---- tall-skinny passes ------------------------------------------------------------------
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
                  int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask, int tri, const FroSpec *fro = nullptr);
+                 unsigned cond_mask, int tri, const FroSpec *fro = nullptr, double alpha = 1.0, double beta = 0.0);
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
                  int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
-                 const unsigned *cond, unsigned cond_mask, int tri);
+                 const unsigned *cond, unsigned cond_mask, int tri, double alpha = 1.0, double beta = 0.0);
 size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms);
 
 size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
@@ -231,6 +231,28 @@ void gemm_nn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t 
   if (gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri)) return;
   gemm_generic_ex(c, false, false, m, cc, k, 1.0, A, lda, X, ldx, 0.0, Y, ldy, partials, partial_elems, false, cond,
                   cond_mask);
+}
+
+// Y = alpha A X + beta Y / Z = alpha A^T V + beta Z on the TMA kernels (the deflation and
+// re-orthogonalisation products of BRQLP), the generic kernel when an operand is not TMA-addressable.
+void gemm_nn_ab(Ctx &c, int64_t m, int64_t cc, int64_t k, double alpha, const double *A, int64_t lda, const double *X,
+                int64_t ldx, double beta, double *Y, int64_t ldy, double *partials, size_t partial_elems) {
+  if (m <= 0 || cc <= 0) return;
+  if (k > 0 && gemm_nn_tma(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, nullptr, 0, 0, nullptr, alpha,
+                           beta))
+    return;
+  gemm_generic_ex(c, false, false, m, cc, k, alpha, A, lda, X, ldx, beta, Y, ldy, partials, partial_elems, false,
+                  nullptr, 0);
+}
+
+void gemm_tn_ab(Ctx &c, int64_t m, int64_t cc, int64_t k, double alpha, const double *A, int64_t lda, const double *V,
+                int64_t ldv, double beta, double *Z, int64_t ldz, double *partials, size_t partial_elems) {
+  if (k <= 0 || cc <= 0) return;
+  if (m > 0 && gemm_tn_tma(c, m, cc, k, A, lda, V, ldv, Z, ldz, false, partials, partial_elems, nullptr, 0, 0, alpha,
+                           beta))
+    return;
+  gemm_generic_ex(c, true, false, k, cc, m, alpha, A, lda, V, ldv, beta, Z, ldz, partials, partial_elems, false,
+                  nullptr, 0);
 }
 
 void gemm_nn_fro(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
                     double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri, int bal_units,
-                    int ntn, int maxc, double *__restrict__ fro_slots) {
+                    int ntn, int maxc, double *__restrict__ fro_slots, double alpha, double beta) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   // tri == 1: only the upper triangle of the (symmetric) output is wanted -- tiles strictly below
   // the diagonal do nothing (a Gram; consumers read the upper triangle).  tri == 2: the B operand
@@ -161,13 +161,15 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): the warps of column
-  // half wn = 0 hold every A element of the k-tile exactly once in their fragments; only the CTAs
-  // of output column tile 0 count (the other column tiles re-read A).  A compile-time switch: a
-  // runtime one cost the plain NN kernel ~10 % (32 more registers, a branch in the MMA loop).
+  // ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): the two warps of a row
+  // band (wn = 0, 1) hold the same A fragments, so each squares half of them (wn = 0 the m-blocks
+  // 0-1, wn = 1 the m-blocks 2-3: every A element of the k-tile exactly once, the extra FMAs spread
+  // evenly over the warps that meet at every k-tile's barrier); only the CTAs of output column
+  // tile 0 count (the other column tiles re-read A).  A compile-time switch: a runtime one cost
+  // the plain NN kernel ~10 % (32 more registers, a branch in the MMA loop).
   static_assert(!FRO || MODE == 0, "||A||^2 is fused into the NN pass only");
   double fro = 0.0;
-  const bool fro_on = FRO && wn == 0 && (bal || n0 == 0);
+  const bool fro_on = FRO && (bal || n0 == 0);
   for (int it = 0; it < nkt; ++it) {
     const int s = it % STAGES;
     // balanced runs: the unit's tile is in output column tile 0
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
         if (MODE == 0) {
           a0[mb] = sa[(kk * 8 + 2 * cq) * LDA_NN + row];
           a1[mb] = sa[(kk * 8 + 2 * cq + 1) * LDA_NN + row];
-          if (fro_it) {
+          if (fro_it && (mb >> 1) == wn) {
             fro = fma(a0[mb], a0[mb], fro);
             fro = fma(a1[mb], a1[mb], fro);
           }
@@ -246,6 +248,27 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
   if (bal) return;
 
   // ---------------- epilogue: fragment (mb, nb) holds out[row][col], out[row][col+1]
+  // (split-K partials are scaled by the reduce; C = alpha acc + beta C otherwise)
+  if (!part && (alpha != 1.0 || beta != 0.0)) {
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) {
+      const int i = m0 + wm * 32 + mb * 8 + r;
+      if (i >= M) continue;
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int j = n0 + wn * (BN / 2) + nb * 8 + 2 * cq;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e >= N) continue;
+          double *dst = trans ? C + (j + e) + (size_t)i * ldc : C + i + (size_t)(j + e) * ldc;
+          double v = alpha * acc[mb][nb][e];
+          if (beta != 0.0) v = fma(beta, *dst, v);
+          *dst = v;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb) {
     const int i = m0 + wm * 32 + mb * 8 + r;
@@ -280,7 +303,8 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
 __global__ void __launch_bounds__(256) bal_reduce_kernel(int M, int N, int bn, int ntn, int ktiles, int units,
                                                          int maxc, const double *__restrict__ part,
                                                          double *__restrict__ C, int64_t ldc, int trans,
-                                                         const unsigned *cond, unsigned cond_mask) {
+                                                         const unsigned *cond, unsigned cond_mask, double alpha,
+                                                         double beta) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   __shared__ double sm[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -312,7 +336,8 @@ __global__ void __launch_bounds__(256) bal_reduce_kernel(int M, int N, int bn, i
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (q + u < cnt) sum += v[u];
-        if (!trans) C[i + (int64_t)j * ldc] = sum;
+        sum *= alpha;
+        if (!trans) C[i + (int64_t)j * ldc] = beta != 0.0 ? fma(beta, C[i + (int64_t)j * ldc], sum) : sum;
       }
       sm[jj][tx] = sum;
     }
@@ -321,7 +346,10 @@ __global__ void __launch_bounds__(256) bal_reduce_kernel(int M, int N, int bn, i
       const int j = j0 + tx;
       for (int ii = ty; ii < 32; ii += 8) {
         const int ir = i0 + ii;
-        if (ir < M && j < N) C[j + (int64_t)ir * ldc] = sm[tx][ii];
+        if (ir < M && j < N) {
+          double *dst = C + j + (int64_t)ir * ldc;
+          *dst = beta != 0.0 ? fma(beta, *dst, sm[tx][ii]) : sm[tx][ii];
+        }
       }
       __syncthreads();
     }
@@ -499,7 +527,7 @@ BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t parti
 template <int BN, int MODE, bool FRO>
 void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
                  int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
-                 const FroSpec *fro) {
+                 const FroSpec *fro, double alpha, double beta) {
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
   smem_attr((const void *)gemm_tma_kernel<BN, MODE, FRO>, SMEM);
@@ -515,12 +543,12 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
     const unsigned ctas = (unsigned)ceil_div(total, bp.units);
     gemm_tma_kernel<BN, MODE, FRO><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
                                                                      part, cond, mask, 0, bp.units, ntn, bp.maxc,
-                                                                     fslots);
+                                                                     fslots, alpha, beta);
     RQLP_LAUNCHED(c);
     fro_finish(ctas);
     const int grid = (int)std::min<int64_t>(ceil_div(M, 32) * ceil_div(N, 32), (int64_t)c.num_sms * 8);
     bal_reduce_kernel<<<std::max(grid, 1), 256, 0, c.stream>>>(M, N, BN, ntn, ktiles, bp.units, bp.maxc, part, C, ldc,
-                                                                trans ? 1 : 0, cond, mask);
+                                                                trans ? 1 : 0, cond, mask, alpha, beta);
     RQLP_LAUNCHED(c);
     return;
   }
@@ -529,39 +557,40 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
   gemm_tma_kernel<BN, MODE, FRO><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
-                                                                       mask, tri, 0, 1, 1, fslots);
+                                                                       mask, tri, 0, 1, 1, fslots, alpha, beta);
   RQLP_LAUNCHED(c);
   fro_finish((int64_t)grid.x * grid.y * grid.z);
-  if (S > 1) launch_reduce(c, M, N, S, part, 1.0, 0.0, C, ldc, trans, cond, mask);
+  if (S > 1) launch_reduce(c, M, N, S, part, alpha, beta, C, ldc, trans, cond, mask);
 }
 
 template <int BN, int MODE>
 void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
                int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
-               const FroSpec *fro) {
+               const FroSpec *fro, double alpha, double beta) {
   if constexpr (MODE == 0) {
     if (fro) {
-      launch_bn_t<BN, 0, true>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro);
+      launch_bn_t<BN, 0, true>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta);
       return;
     }
   }
-  launch_bn_t<BN, MODE, false>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, nullptr);
+  launch_bn_t<BN, MODE, false>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, nullptr, alpha,
+                               beta);
 }
 
 template <int MODE>
 void dispatch(Ctx &c, int bn, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
               int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
-              const FroSpec *fro = nullptr) {
+              const FroSpec *fro, double alpha, double beta) {
   switch (bn) {
-    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
-    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro); break;
+    case 16: launch_bn<16, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 32: launch_bn<32, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 48: launch_bn<48, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 64: launch_bn<64, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 80: launch_bn<80, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 96: launch_bn<96, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 112: launch_bn<112, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    case 128: launch_bn<128, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
+    default: launch_bn<144, MODE>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta); break;
   }
 }
 
@@ -612,11 +641,11 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
 
 bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
                     int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                    unsigned cond_mask, int tri, const FroSpec *fro, int bn);
+                    unsigned cond_mask, int tri, const FroSpec *fro, int bn, double alpha, double beta);
 
 bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X, int64_t ldx,
                  double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask, int tri, const FroSpec *fro) {
+                 unsigned cond_mask, int tri, const FroSpec *fro, double alpha, double beta) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
   static const bool fro_off = env_off("RQLP_FRO_FUSED");   // measurement switch: separate ||A||^2 pass
   if (fro && (cond || tri || fro_off)) return false;
@@ -625,20 +654,20 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
     CUtensorMap probe;   // both column ranges must be TMA-addressable, else one width
     if (make_map(&probe, X + cs.c1 * ldx, k, cc - cs.c1, ldx, BK, cs.bn2) &&
         gemm_nn_tma_bn(c, m, cs.c1, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, 0, fro,
-                       cs.bn1)) {
+                       cs.bn1, alpha, beta)) {
       if (!gemm_nn_tma_bn(c, m, cc - cs.c1, k, A, lda, X + cs.c1 * ldx, ldx, Y + cs.c1 * ldy, ldy, partials,
-                          partial_elems, cond, cond_mask, 0, nullptr, cs.bn2))
+                          partial_elems, cond, cond_mask, 0, nullptr, cs.bn2, alpha, beta))
         throw CudaError("gemm_nn_tma: second column range not launchable");
       return true;
     }
   }
   return gemm_nn_tma_bn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri, fro,
-                        choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms));
+                        choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms), alpha, beta);
 }
 
 bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
                     int64_t ldx, double *Y, int64_t ldy, double *partials, size_t partial_elems, const unsigned *cond,
-                    unsigned cond_mask, int tri, const FroSpec *fro, int bn) {
+                    unsigned cond_mask, int tri, const FroSpec *fro, int bn, double alpha, double beta) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, m, k, lda, LDA_NN, BK)) return false;
   if (!make_map(&mb, X, k, cc, ldx, BK, bn)) return false;
@@ -654,17 +683,18 @@ bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, i
                                       : tiles * ceil_div(ktiles, ceil_div(ktiles, S));
     if (ctas > fro->cap) return false;
   }
-  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri, bp, fro);
+  dispatch<0>(c, bn, ma, mb, (int)m, (int)cc, (int)ktiles, S, Y, ldy, false, partials, cond, cond_mask, tri, bp, fro,
+              alpha, beta);
   return true;
 }
 
 bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
                     int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
-                    const unsigned *cond, unsigned cond_mask, int tri, int bn);
+                    const unsigned *cond, unsigned cond_mask, int tri, int bn, double alpha, double beta);
 
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
                  double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
-                 unsigned cond_mask, int tri) {
+                 unsigned cond_mask, int tri, double alpha, double beta) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
   const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(m, BK)) : ColSplit();
   if (cs.c1 > 0) {
@@ -672,20 +702,20 @@ bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
     double *Z2 = trans_out ? Z + cs.c1 : Z + cs.c1 * ldz;
     if (make_map(&probe, V + cs.c1 * ldv, m, cc - cs.c1, ldv, BK, cs.bn2) &&
         gemm_tn_tma_bn(c, m, cs.c1, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask, 0,
-                       cs.bn1)) {
+                       cs.bn1, alpha, beta)) {
       if (!gemm_tn_tma_bn(c, m, cc - cs.c1, k, A, lda, V + cs.c1 * ldv, ldv, Z2, ldz, trans_out, partials,
-                          partial_elems, cond, cond_mask, 0, cs.bn2))
+                          partial_elems, cond, cond_mask, 0, cs.bn2, alpha, beta))
         throw CudaError("gemm_tn_tma: second column range not launchable");
       return true;
     }
   }
   return gemm_tn_tma_bn(c, m, cc, k, A, lda, V, ldv, Z, ldz, trans_out, partials, partial_elems, cond, cond_mask, tri,
-                        choose_bn_mk(k, cc, ceil_div(m, BK), c.num_sms));
+                        choose_bn_mk(k, cc, ceil_div(m, BK), c.num_sms), alpha, beta);
 }
 
 bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V,
                     int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
-                    const unsigned *cond, unsigned cond_mask, int tri, int bn) {
+                    const unsigned *cond, unsigned cond_mask, int tri, int bn, double alpha, double beta) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, m, k, lda, BK, BM)) return false;
   if (!make_map(&mb, V, m, cc, ldv, BK, bn)) return false;
@@ -701,7 +731,8 @@ bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, i
   BalPlan bp;
   if (tri == 0 && partials && !balanced_disabled())
     bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
-  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri, bp);
+  dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri, bp,
+              nullptr, alpha, beta);
   return true;
 }
 

@@ -203,6 +203,11 @@ void gemm_tn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t 
              int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
              const unsigned *cond = nullptr, unsigned cond_mask = 0, int tri = 0);
 size_t gemm_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms);
+// Y (m x cc) = alpha A X + beta Y (A m x k) and Z (k x cc) = alpha A^T V + beta Z (A m x k, V m x cc)
+void gemm_nn_ab(Ctx &c, int64_t m, int64_t cc, int64_t k, double alpha, const double *A, int64_t lda, const double *X,
+                int64_t ldx, double beta, double *Y, int64_t ldy, double *partials, size_t partial_elems);
+void gemm_tn_ab(Ctx &c, int64_t m, int64_t cc, int64_t k, double alpha, const double *A, int64_t lda, const double *V,
+                int64_t ldv, double beta, double *Z, int64_t ldz, double *partials, size_t partial_elems);
 
 // ---- small dense (dense.cu) ----
 void launch_copy(Ctx &c, int64_t rows, int64_t cols, const double *S, int64_t lds, double *D, int64_t ldd,
