@@ -397,14 +397,15 @@ def main():
     # No host synchronisation inside the timed loop: the host enqueues step i+1 while the device
     # runs step i, so the per-step event pairs measure device time (the host's per-call cost is
     # in the e2e number).  The stage events are those of the last timed step.
-    for name, ms in handle.timing():
+    timing_list = handle.timing()
+    for name, ms in timing_list:
         stage_ms.setdefault(name, []).append(ms)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), group, dev)
     ms_per_step = total_ms / args.steps
     flags = handle.sync()
 
-    # ---- A-pass roofline (the dominant kernel: 92-97% of the flops).  Algorithmic A-pass flops per
+    # ---- A-pass roofline.  All A-passes together (92-97% of the flops): algorithmic A-pass flops per
     # width-l-equivalent pass on this rank (2 m_loc n l; BRQLP: the width-l sketch + (2q+1)
     # width-b_j passes per block, the same total) / the mean per-pass CUDA-event duration inside the
     # timed region (stage events of the last timed step, on the library's stream); max over ranks.
@@ -413,20 +414,48 @@ def main():
     pass_ms = max_over_ranks(pass_ms_loc, group, dev) if pass_names else 0.0
     flops_pass = 2.0 * m_loc * c.n * c.l
     bytes_pass = 8.0 * (m_loc * c.n + m_loc * c.l + c.n * c.l)
-    roof = None
+    apass = None
     if pass_ms > 0:
         mean_pass_ms = pass_ms / passes(c)
-        ach = flops_pass / (mean_pass_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+        apass = {"tflops_per_gpu": round(flops_pass / (mean_pass_ms * 1e-3) / 1e12, 3),
+                 "mean_width_l_pass_ms": round(mean_pass_ms, 4), "apass_ms_per_step": round(pass_ms, 4)}
+    # The dominant kernel's roofline: RQLP/ERQLP -- the width-l pass kernel (every A-pass);
+    # BRQLP -- the width-b block pass (gemm_tma_kernel<b, TN>: A^(j-1)^T V_j and V_j^T A, 2 of the 3
+    # passes of each full block, ~46 % of C4's step), its mean CUDA-event duration over the full
+    # blocks of the last timed step.
+    roof = None
+    if c.b is not None:
+        h_full = c.l // c.b
+        tn = [ms for nm, ms in timing_list if nm in ("pass_block_AtV", "pass_block_project")]
+        full = []    # per full block: q A^T V passes, 1 V^T A pass (q = 0 batches B = V^T A: none)
+        for nm, per in (("pass_block_AtV", c.q), ("pass_block_project", 1)):
+            xs = [ms for n2, ms in timing_list if n2 == nm]
+            full += xs[:h_full * per]
+        if full:
+            kms = max_over_ranks(sum(full) / len(full), group, dev)
+            kflops = 2.0 * m_loc * c.n * c.b
+            kbytes = 8.0 * (m_loc * c.n + m_loc * c.b + c.n * c.b)
+            ach = kflops / (kms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": round(ach / FP64_DMMA_PEAK_TFLOPS, 4),
+                    "traffic": load_traffic(c.name) if world == 1 else None,
+                    "kernel": f"gemm_tma_kernel<{c.b}, TN>: the width-b BRQLP block pass (Z = A^T V_j, B_j = V_j^T A), "
+                              "incl. its split-K reduce; mean CUDA-event time over the full blocks",
+                    "algorithmic_flops_per_launch": kflops, "algorithmic_bytes_per_launch": kbytes,
+                    "mean_launch_ms": round(kms, 4), "launches_per_step": len(full) + (len(tn) - len(full))}
+    if roof is None and apass:
+        ach = apass["tflops_per_gpu"]
+        roof = {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(ach / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": load_traffic(c.name) if world == 1 else None,
-                "kernel": "A-pass: FP64 DMMA GEMM gemm_tma_kernel (Y=AX and B=V^T A / A^T V, incl. split-K "
-                          "reduce); achieved = algorithmic A-pass flops / summed pass event time (per GPU)",
+                "kernel": "gemm_tma_kernel: the width-l A-pass (Y = A X, B = V^T A / A^T V), incl. its split-K reduce; "
+                          "mean CUDA-event time per pass",
                 "algorithmic_flops_per_launch": flops_pass, "algorithmic_bytes_per_launch": bytes_pass,
-                "mean_pass_ms": round(mean_pass_ms, 4), "apass_ms_per_step": round(pass_ms, 4),
-                "peak_source": "measured DMMA m8n8k4 FP64 microbenchmark (tools/microbench/fp64_peak.cu, "
-                               "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
-                "hbm_frac": round(bytes_pass / (mean_pass_ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6540.8),
-                                  4)}
+                "mean_launch_ms": apass["mean_width_l_pass_ms"]}
+    if roof:
+        roof["peak_source"] = ("measured DMMA m8n8k4 FP64 microbenchmark (tools/microbench/fp64_peak.cu, "
+                               "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry")
+        roof["hbm_frac"] = round(roof["algorithmic_bytes_per_launch"] / (roof["mean_launch_ms"] * 1e-3) / 1e9
+                                 / measured_peaks().get("hbm_gbs", 6540.8), 4)
     # whole factorisation: the algorithmic A-pass flops of the step (the roofline-defining work)
     # over the step time, against the N-GPU FP64 peak (BASELINE's "slower of bytes@8TB/s and flops@peak")
     whole_flops = passes(c) * 2.0 * cg.m * c.n * c.l
@@ -478,7 +507,7 @@ def main():
                 "data": "synthetic: A = U diag(sigma) V^T (+noise), Haar U, V from torch.linalg.qr of seeded "
                         "Gaussians; Omega from Philox4x64-10 (DESIGN.md §4)",
                 "config": config_dict(c, world, scaling, cg.m),
-                "apass_tflops_per_gpu": roof["achieved"] if roof else None,
+                "apass": apass,
                 "tflops_effective": whole["tflops"],
                 "roofline": roof, "roofline_whole_factorisation": whole, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(), "step_ms": [round(t, 4) for t in step_ms],

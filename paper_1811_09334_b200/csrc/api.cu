@@ -516,23 +516,33 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
-  // reorth: Vj <- qr(Vj - V_<j (V_<j^T Vj))  (eq. (18))
-  // Alg.3 l.5, applied twice ("twice is enough", reading R28): identical in exact arithmetic
-  // when V_j has a component outside span(V_<j) (the second projection removes nothing), and
-  // the only way to keep Q orthonormal when it has (almost) none -- a block beyond rank(A), whose
-  // first residual is rounding noise (one pass then returns directions far from orthogonal to
-  // V_<j, as the literal line does in exact arithmetic: qr(0)).
-  auto reorth = [&](int64_t c0, int64_t bj) {
-    if (c0 == 0) return;
+  // Alg.3 l.4-5: V_j = qr(Y_j), then V_j <- qr(V_j - V_<j (V_<j^T V_j)) (eq. (18)), the latter
+  // applied twice ("twice is enough", reading R28: identical in exact arithmetic when V_j has a
+  // component outside span(V_<j) -- the second projection removes nothing -- and the only way to
+  // keep Q orthonormal when it has (almost) none: a block beyond rank(A), whose first residual is
+  // rounding noise).  Computed as block CGS2 on Y_j itself (overwritten):
+  //   W = Y_j - V_<j (V_<j^T Y_j),  V_j = qr1(W)  (one CholeskyQR pass: only its span is used),
+  //   V_j <- V_j - V_<j (V_<j^T V_j), V_j = qr(V_j)  (CholeskyQR2),
+  // equal to the literal sequence in exact arithmetic: qr(Y_j) = Y_j R^-1 with R upper triangular
+  // and R_ii > 0, so P(Y_j R^-1) = (P Y_j) R^-1 spans the same space with the same R_ii > 0
+  // normalisation.  3 CholeskyQR passes where the literal form takes 6 (C4: 12 -> 6 m x b passes
+  // per block).  The first block has nothing to project against: V_1 = qr(Y_1).
+  auto block_orth = [&](double *Yj, int64_t c0, int64_t bj) {
     double *Vj = P.V + c0 * ldm;
-    c.mark("b_other");
-    for (int pass = 0; pass < 2; ++pass) {
-      gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);   // C = V_<j^T Vj
-      allreduce_sum(c, P.C, LL * bj);
-      gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems);   // Vj -= V_<j C
-      launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
-      orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);
+    if (c0 == 0) {
+      orth(c, P.orth, m, bj, Yj, ldm, Vj, ldm, nullptr, 0, sh);
+      return;
     }
+    c.mark("b_other");
+    gemm_tn(c, m, bj, c0, P.V, ldm, Yj, ldm, P.C, LL, false, P.part, P.part_elems);        // C = V_<j^T Y_j
+    allreduce_sum(c, P.C, LL * bj);
+    gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Yj, ldm, P.part, P.part_elems);  // W = Y_j - V_<j C
+    orth(c, P.orth, m, bj, Yj, ldm, Vj, ldm, nullptr, 0, sh, true);                         // span of W
+    gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);        // C = V_<j^T V_j
+    allreduce_sum(c, P.C, LL * bj);
+    gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems);  // V_j -= V_<j C
+    launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
+    orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);                            // CholeskyQR2
   };
   // q = 0 (NEXT-4): the range finder needs no A-pass per block, so every V_j is built first
   // and ONE batched pass B = V^T A replaces the h per-block projections; the deflation
@@ -541,8 +551,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   if (two_pass) {
     for (int64_t j = 0; j < h_blocks; ++j) {
       const int64_t c0 = j * b, bj = std::min<int64_t>(b, l - c0);
-      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, P.V + c0 * ldm, ldm, nullptr, 0, sh);  // l.4
-      reorth(c0, bj);                                                                       // l.5
+      block_orth(P.Y + c0 * ldm, c0, bj);                                                   // l.4-5
     }
     c.mark("b_other");
     gemm_tn(c, m, l, n, A, lda, P.V, ldm, B, LL, true, P.part, P.part_elems);           // all V_j^T A
@@ -563,8 +572,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       c.mark("pass_block_sketch");
     }
     if (!two_pass) {
-      orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);              // l.4
-      reorth(c0, bj);                                                                      // l.5
+      block_orth(P.Y + c0 * ldm, c0, bj);                                                  // l.4-5
       for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
         if (h->dbgVP) launch_copy(c, m, bj, Vj, ldm, h->dbgVP + (it * l + c0) * h->ldVP, h->ldVP, false);
         c.mark("b_other");
@@ -587,8 +595,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
           gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.D, LL, 1.0, P.Y + c0 * ldm, ldm, P.part, P.part_elems);  // Y -= V_<j D
         }
         if (h->dbgYP) launch_copy(c, m, bj, P.Y + c0 * ldm, ldm, h->dbgYP + (it * l + c0) * h->ldYP, h->ldYP, false);
-        orth(c, P.orth, m, bj, P.Y + c0 * ldm, ldm, Vj, ldm, nullptr, 0, sh);
-        reorth(c0, bj);
+        block_orth(P.Y + c0 * ldm, c0, bj);
       }
     }
     // l.6: B_j = Vj^T A^(j-1) = Vj^T A - (Vj^T V_<j) B_<j, formed in the tail's B buffer

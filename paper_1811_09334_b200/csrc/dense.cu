@@ -129,23 +129,82 @@ __global__ void colsumsq_kernel(int64_t rows, int64_t cols, const double *__rest
   }
 }
 
-__global__ void accumulate_parts_kernel(int nparts, const double *part, double *out, int first) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = first ? 0.0 : *out;
-    for (int i = 0; i < nparts; ++i) t += part[i];
-    *out = t;
+// *out (+)= sum of the parts: thread t sums parts t, t + 256, ... in order, then a fixed tree.
+__global__ void __launch_bounds__(256) accumulate_parts_kernel(int nparts, const double *part, double *out, int first) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *out = first ? red[0] : *out + red[0];
 }
 
 }  // namespace
 
+// part[b] = sum of squares of the column range [b cpb, (b+1) cpb) of X: each warp takes a column,
+// 16-byte loads with four accumulation chains (the large-input form: a whole A when the fused
+// ||A||^2 cannot ride on the sketch pass -- its tile width or alignment -- read at HBM speed).
+__global__ void __launch_bounds__(256) colrange_sumsq_kernel(int64_t rows, int64_t cols, int64_t cpb,
+                                                             const double *__restrict__ X, int64_t ldx, double *part) {
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * cpb, j1 = min(cols, j0 + cpb);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const bool vec = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  for (int64_t j = j0 + warp; j < j1; j += 8) {
+    const double *x = X + j * ldx;
+    int64_t i = 0;
+    if (vec) {
+      const double2 *x2 = reinterpret_cast<const double2 *>(x);
+      const int64_t h = rows >> 1;
+      int64_t t = lane;
+      for (; t + 32 < h; t += 64) {
+        const double2 a = x2[t], b = x2[t + 32];
+        s0 = fma(a.x, a.x, s0);
+        s1 = fma(a.y, a.y, s1);
+        s2 = fma(b.x, b.x, s2);
+        s3 = fma(b.y, b.y, s3);
+      }
+      if (t < h) {
+        const double2 a = x2[t];
+        s0 = fma(a.x, a.x, s0);
+        s1 = fma(a.y, a.y, s1);
+      }
+      i = 2 * h;
+    }
+    for (int64_t r = i + lane; r < rows; r += 32) s2 = fma(x[r], x[r], s2);
+  }
+  double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
 // *out (+)= ||X||_F^2 (X rows x cols, ld), deterministic fixed-order reduction; part >= 1024 doubles.
 void fro2_accumulate(Ctx &c, int64_t rows, int64_t cols, const double *X, int64_t ldx, double *part, double *out,
                      bool first) {
-  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cols, 1024));
-  colsumsq_kernel<<<nb, 256, 0, c.stream>>>(rows, cols, X, ldx, part);
+  int nb;
+  if (rows * cols >= ((int64_t)1 << 22)) {   // large: column ranges over ~8 CTAs per SM
+    nb = (int)std::max<int64_t>(1, std::min<int64_t>({cols, (int64_t)c.num_sms * 8, 1024}));
+    const int64_t cpb = ceil_div(cols, nb);
+    nb = (int)ceil_div(cols, cpb);
+    colrange_sumsq_kernel<<<nb, 256, 0, c.stream>>>(rows, cols, cpb, X, ldx, part);
+  } else {
+    nb = (int)std::max<int64_t>(1, std::min<int64_t>(cols, 1024));
+    colsumsq_kernel<<<nb, 256, 0, c.stream>>>(rows, cols, X, ldx, part);
+  }
   RQLP_LAUNCHED(c);
-  accumulate_parts_kernel<<<1, 32, 0, c.stream>>>(nb, part, out, first ? 1 : 0);
+  accumulate_parts_kernel<<<1, 256, 0, c.stream>>>(nb, part, out, first ? 1 : 0);
   RQLP_LAUNCHED(c);
 }
 

@@ -30,6 +30,9 @@ void launch_reduce(Ctx &c, int64_t M, int64_t N, int S, const double *part, doub
 namespace {
 
 constexpr int BM = 128, BK = 24, STAGES = 4, NCONS = 8;
+// the ||A||^2 warp makes 9 warps: 3 on one SM sub-partition caps the registers at 168 per thread,
+// which spills the accumulators for BN > 96 -- those passes use a separate ||A||^2 pass
+constexpr int FRO_MAX_BN = 96;
 constexpr int LDA_NN = BM + 2;  // doubles
 constexpr int A_TILE_BYTES_NN = ((BK * LDA_NN * 8 + 127) / 128) * 128;
 constexpr int A_TILE_BYTES_TN = BM * BK * 8;
@@ -74,7 +77,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 // MODE 0 = NN, 1 = TN.  Output element (i, j) of the (M x N) product goes to
 //   part (split-K slice, M x N contiguous)  or  C[i + j ldc]  or (trans) C[j + i ldc].
 template <int BN, int MODE, bool FRO>
-__global__ void __launch_bounds__(NCONS * 32, 1)
+__global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
                     double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri, int bal_units,
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
+      mbar_init(&empty[s], NCONS + (FRO ? 1 : 0));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -152,6 +155,42 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
     for (int it = 0; it < STAGES - 1 && it < nkt; ++it) issue(it);
   }
 
+  // ---------------- ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): a 9th
+  // warp squares every staged A tile (rows 0..127 of the 130-row box; OOB rows and columns are
+  // zero-filled) and releases the stage like a consumer; only the CTAs of output column tile 0
+  // count (the other column tiles re-read A).  Measured: the same FMAs inside the consumer warps'
+  // MMA loop cost the pass ~7 % (register growth, a broken load/MMA schedule); a compile-time
+  // switch, as a runtime one cost the plain NN kernel ~10 %.
+  static_assert(!FRO || MODE == 0, "||A||^2 is fused into the NN pass only");
+  if (FRO && warp == NCONS) {
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+    const bool fro_on = bal || n0 == 0;
+    for (int it = 0; it < nkt; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      // balanced runs: count the unit if its tile is in output column tile 0
+      if (fro_on && (!bal || ((u0 + it) / ktiles_total) % ntn == 0)) {
+        const double *sa = reinterpret_cast<const double *>(smem + s * STAGE_BYTES);
+#pragma unroll 4
+        for (int k = 0; k < BK; ++k) {
+          const double *colk = sa + k * LDA_NN;
+          const double x0 = colk[lane], x1 = colk[lane + 32], x2 = colk[lane + 64], x3 = colk[lane + 96];
+          f0 = fma(x0, x0, f0);
+          f1 = fma(x1, x1, f1);
+          f2 = fma(x2, x2, f2);
+          f3 = fma(x3, x3, f3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    double f = (f0 + f1) + (f2 + f3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    if (lane == 0) fro_slots[blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)] = f;
+    return;
+  }
+
   // ---------------- consumers: 8 warps, 4 (M) x 2 (N), warp tile 32 x BN/2
   const int wm = warp & 3, wn = warp >> 2;
   const int r = lane >> 2, cq = lane & 3;
@@ -161,19 +200,8 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): the two warps of a row
-  // band (wn = 0, 1) hold the same A fragments, so each squares half of them (wn = 0 the m-blocks
-  // 0-1, wn = 1 the m-blocks 2-3: every A element of the k-tile exactly once, the extra FMAs spread
-  // evenly over the warps that meet at every k-tile's barrier); only the CTAs of output column
-  // tile 0 count (the other column tiles re-read A).  A compile-time switch: a runtime one cost
-  // the plain NN kernel ~10 % (32 more registers, a branch in the MMA loop).
-  static_assert(!FRO || MODE == 0, "||A||^2 is fused into the NN pass only");
-  double fro = 0.0;
-  const bool fro_on = FRO && (bal || n0 == 0);
   for (int it = 0; it < nkt; ++it) {
     const int s = it % STAGES;
-    // balanced runs: the unit's tile is in output column tile 0
-    const bool fro_it = fro_on && (!bal || ((u0 + it) / ktiles_total) % ntn == 0);
     if (threadIdx.x == 0 && it + STAGES - 1 < nkt) {
       // refill the slot consumed at iteration it-1 once every warp has released it
       if (it >= 1) mbar_wait(&empty[(it - 1) % STAGES], ((it - 1) / STAGES) & 1);
@@ -191,10 +219,6 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
         if (MODE == 0) {
           a0[mb] = sa[(kk * 8 + 2 * cq) * LDA_NN + row];
           a1[mb] = sa[(kk * 8 + 2 * cq + 1) * LDA_NN + row];
-          if (fro_it && (mb >> 1) == wn) {
-            fro = fma(a0[mb], a0[mb], fro);
-            fro = fma(a1[mb], a1[mb], fro);
-          }
         } else {
           const double2 v = *reinterpret_cast<const double2 *>(sa + row * BK + kk * 8 + 2 * cq);
           a0[mb] = v.x;
@@ -230,19 +254,6 @@ __global__ void __launch_bounds__(NCONS * 32, 1)
           acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
         }
       }
-    }
-  }
-  if (FRO) {   // per-CTA partial of ||A||_F^2, fixed-order reduction
-    __shared__ double fro_red[NCONS];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-    if (lane == 0) fro_red[warp] = fro;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < NCONS; ++w) t += fro_red[w];
-      fro_slots[blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)] = t;
     }
   }
   if (bal) return;
@@ -541,7 +552,7 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
     const int ntn = (int)ceil_div(N, BN);
     const int64_t total = (int64_t)ktiles * ntn * ceil_div(M, BM);
     const unsigned ctas = (unsigned)ceil_div(total, bp.units);
-    gemm_tma_kernel<BN, MODE, FRO><<<ctas, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
+    gemm_tma_kernel<BN, MODE, FRO><<<ctas, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
                                                                      part, cond, mask, 0, bp.units, ntn, bp.maxc,
                                                                      fslots, alpha, beta);
     RQLP_LAUNCHED(c);
@@ -555,7 +566,7 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
   int kps = (int)ceil_div(ktiles, S);
   S = (int)ceil_div(ktiles, kps);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
-  gemm_tma_kernel<BN, MODE, FRO><<<grid, NCONS * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
+  gemm_tma_kernel<BN, MODE, FRO><<<grid, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
                                                                        mask, tri, 0, 1, 1, fslots, alpha, beta);
   RQLP_LAUNCHED(c);
@@ -567,7 +578,7 @@ template <int BN, int MODE>
 void launch_bn(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
                int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
                const FroSpec *fro, double alpha, double beta) {
-  if constexpr (MODE == 0) {
+  if constexpr (MODE == 0 && BN <= FRO_MAX_BN) {
     if (fro) {
       launch_bn_t<BN, 0, true>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta);
       return;
@@ -651,18 +662,33 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (fro && (cond || tri || fro_off)) return false;
   const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(k, BK)) : ColSplit();
   if (cs.c1 > 0) {
+    // the ||A||^2 goes with one column range (each reads all of A), one whose width can carry it
+    const FroSpec *f1 = nullptr, *f2 = nullptr;
+    if (fro) {
+      if (cs.bn2 <= FRO_MAX_BN) f2 = fro;
+      else if (cs.bn1 <= FRO_MAX_BN) f1 = fro;
+      else return false;
+    }
     CUtensorMap probe;   // both column ranges must be TMA-addressable, else one width
     if (make_map(&probe, X + cs.c1 * ldx, k, cc - cs.c1, ldx, BK, cs.bn2) &&
-        gemm_nn_tma_bn(c, m, cs.c1, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, 0, fro,
+        gemm_nn_tma_bn(c, m, cs.c1, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, 0, f1,
                        cs.bn1, alpha, beta)) {
       if (!gemm_nn_tma_bn(c, m, cc - cs.c1, k, A, lda, X + cs.c1 * ldx, ldx, Y + cs.c1 * ldy, ldy, partials,
-                          partial_elems, cond, cond_mask, 0, nullptr, cs.bn2, alpha, beta))
-        throw CudaError("gemm_nn_tma: second column range not launchable");
+                          partial_elems, cond, cond_mask, 0, f2, cs.bn2, alpha, beta)) {
+        // (only the ||A||^2 slot capacity can refuse it) plain range + a separate ||A||^2 pass
+        if (!f2 || !gemm_nn_tma_bn(c, m, cc - cs.c1, k, A, lda, X + cs.c1 * ldx, ldx, Y + cs.c1 * ldy, ldy, partials,
+                                   partial_elems, cond, cond_mask, 0, nullptr, cs.bn2, alpha, beta))
+          throw CudaError("gemm_nn_tma: second column range not launchable");
+        fro2_accumulate(c, m, k, A, lda, f2->slots, f2->out, !f2->accumulate);
+      }
       return true;
     }
+    if (f1) return false;   // (the first range was not launched)
   }
-  return gemm_nn_tma_bn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri, fro,
-                        choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms), alpha, beta);
+  const int bn = choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms);
+  if (fro && bn > FRO_MAX_BN) return false;
+  return gemm_nn_tma_bn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri, fro, bn,
+                        alpha, beta);
 }
 
 bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *X,
