@@ -26,6 +26,9 @@ namespace rqlpk {
 
 void launch_reduce(Ctx &c, int64_t M, int64_t N, int S, const double *part, double alpha, double beta, double *C,
                    int64_t ldc, bool trans, const unsigned *cond, unsigned cond_mask);
+void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                     int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc, double *partials,
+                     size_t partial_elems, bool trans_out, const unsigned *cond, unsigned cond_mask);
 
 namespace {
 
@@ -646,6 +649,11 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
       need(M, cs.c1, ktiles, cs.bn1);
       need(M, cc - cs.c1, ktiles, cs.bn2);
     }
+    const int64_t c1 = (cc / FRO_MAX_BN) * FRO_MAX_BN;   // the ||A||^2-carrying split of the sketch
+    if (mode == 0 && c1 > 0) {
+      need(M, c1, ktiles, FRO_MAX_BN);
+      if (c1 < cc) need(M, cc - c1, ktiles, choose_bn_mk(M, cc - c1, ktiles, num_sms));
+    }
   }
   return best;
 }
@@ -686,7 +694,20 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
     if (f1) return false;   // (the first range was not launched)
   }
   const int bn = choose_bn_mk(m, cc, ceil_div(k, BK), c.num_sms);
-  if (fro && bn > FRO_MAX_BN) return false;
+  if (fro && bn > FRO_MAX_BN) {
+    // every width of the plan is too wide for the ||A||^2 warp: the first floor(cc / 96) * 96 columns
+    // in 96-wide tiles carrying it, the rest as a plain pass (C2: 96 + 14, C3: 2 x 96 + 80 -- no
+    // padded columns; the extra A read of a compute-bound pass is hidden)
+    const int64_t c1 = (cc / FRO_MAX_BN) * FRO_MAX_BN;
+    if (!gemm_nn_tma_bn(c, m, c1, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, 0, fro,
+                        FRO_MAX_BN, alpha, beta))
+      return false;
+    if (c1 < cc && !gemm_nn_tma(c, m, cc - c1, k, A, lda, X + c1 * ldx, ldx, Y + c1 * ldy, ldy, partials,
+                                partial_elems, cond, cond_mask, 0, nullptr, alpha, beta))
+      gemm_generic_ex(c, false, false, m, cc - c1, k, alpha, A, lda, X + c1 * ldx, ldx, beta, Y + c1 * ldy, ldy,
+                      partials, partial_elems, false, cond, cond_mask);
+    return true;
+  }
   return gemm_nn_tma_bn(c, m, cc, k, A, lda, X, ldx, Y, ldy, partials, partial_elems, cond, cond_mask, tri, fro, bn,
                         alpha, beta);
 }
