@@ -125,7 +125,7 @@ Ctx make_ctx(rqlp_handle_t h) {
   c.ev_fork = h->ev_fork;
   c.ev_join = h->ev_join;
   if (getenv("RQLP_ENGINE_TRACE")) {
-    if (!g_trace) cudaMalloc(&g_trace, 4 * 4096 * sizeof(unsigned long long));
+    if (!g_trace) cudaMalloc(&g_trace, 16 * 4096 * sizeof(unsigned long long));
     c.trace = g_trace;
   }
   return c;

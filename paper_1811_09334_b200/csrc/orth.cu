@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
                                                           unsigned dep_bit, unsigned *flag_word, const unsigned *cond,
                                                           unsigned cond_mask, int near_id, double shift_m,
                                                           unsigned *shift_word, unsigned shift_bit,
-                                                          const double *maxdev, int nmaxdev, int zero_cond) {
+                                                          const double *maxdev, int nmaxdev, int zero_cond,
+                                                          unsigned long long *trace) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   // the first pass of an orth clears the COND word itself (instead of a memset node): no other
   // kernel of the orth has touched it yet, and the bits below are set after barriers
@@ -220,12 +221,19 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         }
       }
     };
+    // debug (RQLP_ENGINE_TRACE): SM clock at the phases of every block of the first attempt
+    auto stamp = [&](int kb, int ph) {
+      if (trace && attempt == 0 && kb < 32) trace[kb * 4 + ph] = (unsigned long long)clock64();
+    };
+    if (tid == 0) stamp(31, 0);
     if (warp == 0) phase1(0, wkk[0]);
+    if (tid == 0) stamp(31, 1);
 
     __syncthreads();
     for (int kb = 0; kb < nt; ++kb) {
       const int k0 = kb * 8;
       const double *wk = wkk[kb & 1];
+      if (tid == 0) stamp(kb, 0);
       // ---- phase 2: M[T, K] <- M[T, K] W_KK^T for every row tile T != K
       for (int T = warp; T < nt; T += nwarps) {
         if (T == kb) continue;
@@ -240,6 +248,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         M[r + (k0 + 2 * fq + 1) * CB_LD] = c1;
       }
       __syncthreads();
+      if (tid == 0) stamp(kb, 1);
       // ---- phase 3: trailing column tiles Tc > kb.  S part: tiles (Tr >= Tc); W part: Tr <= kb.
       //      Tile 0 is the next diagonal block: warp 0 updates it and then runs phase 1 of block
       //      kb + 1 (lookahead) while warps 1.. do the remaining tiles.
@@ -287,11 +296,13 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
           tile(0);
           __syncwarp();
           phase1(kb + 1, wkk[(kb + 1) & 1]);
+          if (lane == 0) stamp(kb, 3);
         } else {
           for (int t = warp; t < n_s + n_w; t += nwarps - 1) tile(t);
         }
       }
       __syncthreads();
+      if (tid == 0) stamp(kb, 2);
     }
     // breakdown with a shift length given: redo on G + s I, s = 11 (m n + n (n+1)) u tr(G)
     __syncthreads();
@@ -422,7 +433,8 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
   smem_attr((const void *)chol_blk_kernel, CHOL_SMALL * CB_LD * 8);
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
-      near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev, zero_cond);
+      near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev, zero_cond,
+      c.trace ? c.trace + 8 * 4096 : nullptr);
   RQLP_LAUNCHED(c);
 }
 
