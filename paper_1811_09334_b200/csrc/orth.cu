@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
     int ai = tid % hp, bi = tid / hp;
     // the original diagonal first (its loads overlap the matrix's)
     for (int i = tid; i < npad; i += blockDim.x) g0s[i] = i < n ? Gorig[i + (int64_t)i * ldo] + shift : 1.0;
-#pragma unroll 16
+#pragma unroll 4
     for (int e = tid; e < tot; e += blockDim.x) {
       const int r = 2 * ai, c = bi;
       ai += da;
@@ -163,63 +163,57 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   int *dep_att = dep;
   for (int attempt = 0;; ++attempt) {
     const int fr = lane >> 2, fq = lane & 3;  // DMMA fragment coordinates
-    // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf]
+    // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf].
+    // Lane (i, q) = (lane / 4, lane % 4) holds D(i, 2q..2q+1) and W(i, 2q..2q+1) of the 8 x 8 block;
+    // a pivot is 6 shuffles, one reciprocal and 4 predicated FMAs, in a ROLLED loop: the code is
+    // executed once per block and its first execution in a launch fetches every instruction from
+    // L2 (measured: the earlier fully unrolled form -- 17 shuffles per pivot, two inlined copies,
+    // ~840 instructions each -- spent 36k cycles, 18 us, in its first call on i-cache misses).
     auto phase1 = [&](int kb, double *wk) {
       const int k0 = kb * 8;
-      const int i = lane & 7;
-      double d[8], w[8], g0[8], piv[8], sv[8];  // lane i: row i of the block and of W_KK
-  #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int r = k0 + i, cc = k0 + j;
-        d[j] = r >= cc ? M[r + cc * CB_LD] : M[cc + r * CB_LD];
-        w[j] = (i == j) ? 1.0 : 0.0;
-        g0[j] = g0s[cc];
-      }
-      // the pivot chain only: shuffles, the reciprocal and FMAs (bookkeeping after the loop)
-      unsigned kinds = 0;
-  #pragma unroll
+      const int i = lane >> 2, q = lane & 3, ca = 2 * q, cb = ca + 1;
+      const int r = k0 + i;
+      double d0 = r >= k0 + ca ? M[r + (k0 + ca) * CB_LD] : M[(k0 + ca) + r * CB_LD];
+      double d1 = r >= k0 + cb ? M[r + (k0 + cb) * CB_LD] : M[(k0 + cb) + r * CB_LD];
+      double w0 = (i == ca) ? 1.0 : 0.0, w1 = (i == cb) ? 1.0 : 0.0;
+  #pragma unroll 1
       for (int p = 0; p < 8; ++p) {
-        const double draw = __shfl_sync(0xffffffffu, d[p], p);
+        const bool odd = p & 1;
+        const double draw = __shfl_sync(0xffffffffu, odd ? d1 : d0, p * 4 + (p >> 1));   // D(p, p)
+        const double dip = __shfl_sync(0xffffffffu, odd ? d1 : d0, i * 4 + (p >> 1));    // D(i, p)
+        const double dp0 = __shfl_sync(0xffffffffu, d0, p * 4 + q), dp1 = __shfl_sync(0xffffffffu, d1, p * 4 + q);
+        const double wp0 = __shfl_sync(0xffffffffu, w0, p * 4 + q), wp1 = __shfl_sync(0xffffffffu, w1, p * 4 + q);
+        const double g0 = g0s[k0 + p];
+        unsigned kind = 0;
         double pv = draw;
-        if (!isfinite(draw)) { kinds |= 2u << (2 * p); pv = 1.0; }
-        else if (dep_att && !(draw > CHOL_DEP * g0[p])) { kinds |= 1u << (2 * p); pv = 1.0; }
-        else if (!(draw > CHOL_BREAK * g0[p])) { kinds |= 2u << (2 * p); pv = 1.0; }
-        piv[p] = pv;
+        if (!isfinite(draw)) { kind = 2; pv = 1.0; }
+        else if (dep_att && !(draw > CHOL_DEP * g0)) { kind = 1; pv = 1.0; }
+        else if (!(draw > CHOL_BREAK * g0)) { kind = 2; pv = 1.0; }
         const double pinv = fast_rcp(pv);
-        sv[p] = d[p];                                   // final S value L_ip d_p (i > p)
-        const double l = (i > p) ? d[p] * pinv : 0.0;  // L_ip (row i of the block)
-  #pragma unroll
-        for (int j = p + 1; j < 8; ++j) d[j] = fma(-l, __shfl_sync(0xffffffffu, d[j], p), d[j]);
-  #pragma unroll
-        for (int t = 0; t <= p; ++t) w[t] = fma(-l, __shfl_sync(0xffffffffu, w[t], p), w[t]);
-      }
-      if (lane < 8) {
-  #pragma unroll
-        for (int p = 0; p < 8; ++p)
-          if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
-        const int kg = k0 + i;  // lane i records pivot i
-        double pv = piv[0], dr = d[0];
-  #pragma unroll
-        for (int p = 1; p < 8; ++p) if (i == p) { pv = piv[p]; dr = d[p]; }
-        // a numerically dependent column (pivot <= 1e-15 of its diagonal before any shift):
-        // reported as RQLP_FLAG_RANK_DEFICIENT whether or not the column is completed here
-        if (attempt == 0 && kg < n && !(dr > CHOL_DEP * g0s[kg]) && !isnan(dr)) s_tiny = 1;
-        dpiv[kg] = pv;
-        dinv[kg] = fast_rcp(pv);
-        const unsigned kind = (kinds >> (2 * i)) & 3u;
-        if (kg < n) {
-          if (dep_att) dep_att[kg] = kind == 1;
-          if (kind == 1) s_dep = 1;
-          if (kind == 2) s_fail = 1;
+        if (i > p && q == (p >> 1)) M[r + (k0 + p) * CB_LD] = odd ? d1 : d0;   // final S value L_ip d_p
+        const double l = (i > p) ? dip * pinv : 0.0;                            // L_ip
+        if (ca > p) d0 = fma(-l, dp0, d0);
+        if (cb > p) d1 = fma(-l, dp1, d1);
+        if (ca <= p) w0 = fma(-l, wp0, w0);
+        if (cb <= p) w1 = fma(-l, wp1, w1);
+        if (lane == 0) {   // pivot p's bookkeeping (uniform values)
+          const int kg = k0 + p;
+          // a numerically dependent column (pivot <= 1e-15 of its diagonal before any shift):
+          // reported as RQLP_FLAG_RANK_DEFICIENT whether or not the column is completed here
+          if (attempt == 0 && kg < n && !(draw > CHOL_DEP * g0) && !isnan(draw)) s_tiny = 1;
+          dpiv[kg] = pv;
+          dinv[kg] = pinv;
+          if (kg < n) {
+            if (dep_att) dep_att[kg] = kind == 1;
+            if (kind == 1) s_dep = 1;
+            if (kind == 2) s_fail = 1;
+          }
         }
       }
-      if (lane < 8) {
-  #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          wk[i * 8 + t] = w[t];
-          if (t < i) M[(k0 + t) + (k0 + i) * CB_LD] = w[t];  // W_{k0+i, k0+t} in the upper part
-        }
-      }
+      wk[i * 8 + ca] = w0;
+      wk[i * 8 + cb] = w1;
+      if (ca < i) M[(k0 + ca) + r * CB_LD] = w0;   // W_{k0+i, k0+t} in the upper part
+      if (cb < i) M[(k0 + cb) + r * CB_LD] = w1;
     };
     // debug (RQLP_ENGINE_TRACE): SM clock at the phases of every block of the first attempt
     auto stamp = [&](int kb, int ph) {
@@ -321,19 +315,27 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
     load(shift);
     __syncthreads();
   }
-  for (int i = tid; i < n; i += blockDim.x) sq[i] = sqrt(dpiv[i]);
+  for (int i = tid; i < n; i += blockDim.x) {
+    sq[i] = sqrt(dpiv[i]);
+    dinv[i] = 1.0 / sq[i];   // (the pivot reciprocals are no longer needed)
+  }
   __syncthreads();
   // outputs: R(c, r) = S_rc / sqrt(d_c) (c < r), R(r, r) = sqrt(d_r), R lower = 0;
-  //          X(r, c) = W_cr / sqrt(d_c) (r < c), X(r, r) = 1 / sqrt(d_r), X lower = 0.
+  //          X(r, c) = W_cr / sqrt(d_c) (r < c), X(r, r) = 1 / sqrt(d_r), X lower = 0
+  // (one reciprocal per column, rolled loops: this code runs once per launch, cold in the i-cache)
+#pragma unroll 1
   for (int r = warp; r < n; r += nwarps)
+#pragma unroll 1
     for (int c = lane; c < n; c += 32) {  // R(c, r): coalesced over c
       double v = 0.0;
-      if (c < r) v = M[r + c * CB_LD] / sq[c];
+      if (c < r) v = M[r + c * CB_LD] * dinv[c];
       else if (c == r) v = sq[r];
       R[c + (int64_t)r * ldr] = v;
     }
+#pragma unroll 1
   for (int c = warp; c < n; c += nwarps) {
-    const double isq = 1.0 / sq[c];
+    const double isq = dinv[c];
+#pragma unroll 1
     for (int r = lane; r < n; r += 32) {  // X(r, c): coalesced over r
       double v = 0.0;
       if (r < c) v = M[r + c * CB_LD] * isq;
