@@ -81,6 +81,7 @@ struct EngineArgs {
   unsigned long long *trace; // optional per-step phase timestamps (CTA 0, thread 0), debugging only
   int *done;                // done[col] = 1 once pivoted (compaction of the non-pivot columns)
   int64_t *perm;
+  int npoll;                 // warps that poll the exchange records (redundantly; warp 0 publishes p)
 };
 
 // Exchange words: gpu-scope relaxed accesses (every word carries its step tag, so no ordering
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
     int p;
     if (GRID) {
       const unsigned tag = (a.epoch << 16) | ((unsigned)j + 1u);
-      if (warp == 0) {
+      if (warp < a.npoll) {
         Best c{-1.0, 0x7fffffff};
         if (a.pivot) {
           // each lane owns records lane, lane+32, ...: issue all loads, re-poll only the stale ones
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
         } else {
           c.i = j;
         }
-        if (lane == 0) s_p = c.i;
+        if (warp == 0 && lane == 0) s_p = c.i;
       }
       __syncthreads();
       p = s_p;
@@ -752,6 +753,14 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
   a.Vst = s.Vst; a.tau = s.tau; a.beta = s.beta; a.rec = s.rec; a.cand = s.cand; a.done = s.done; a.perm = s.perm;
   a.epoch = 0;
   a.trace = c.trace;
+  {  // RQLP_ENGINE_POLL_WARPS (measurement switch): warps polling the exchange records
+    static int np = -1;
+    if (np < 0) {
+      const char *e = getenv("RQLP_ENGINE_POLL_WARPS");
+      np = e ? std::max(1, atoi(e)) : 1;
+    }
+    a.npoll = np;
+  }
   auto smem_for = [&](int64_t owned, bool cached) {
     const int64_t rs = round_up(rows, 2), op = round_up(owned, 2);
     return (size_t)(rs + 3 * op + (cached ? owned * rs : 0)) * 8 + (size_t)owned * 4 + 64;

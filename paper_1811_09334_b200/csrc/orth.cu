@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
                                                           unsigned cond_mask, int near_id, double shift_m,
                                                           unsigned *shift_word, unsigned shift_bit,
                                                           const double *maxdev, int nmaxdev, int zero_cond,
-                                                          unsigned long long *trace) {
+                                                          unsigned long long *trace, int busy) {
   if (cond && ((*cond) & cond_mask) == 0) return;
   // the first pass of an orth clears the COND word itself (instead of a memset node): no other
   // kernel of the orth has touched it yet, and the bits below are set after barriers
@@ -163,64 +163,76 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
   int *dep_att = dep;
   for (int attempt = 0;; ++attempt) {
     const int fr = lane >> 2, fq = lane & 3;  // DMMA fragment coordinates
-    // phase 1 of block kb (warp 0 only): LDL^T of the diagonal block, W_KK into wkk[buf].
-    // Lane (i, q) = (lane / 4, lane % 4) holds D(i, 2q..2q+1) and W(i, 2q..2q+1) of the 8 x 8 block;
-    // a pivot is 6 shuffles, one reciprocal and 4 predicated FMAs, in a ROLLED loop: the code is
-    // executed once per block and its first execution in a launch fetches every instruction from
-    // L2 (measured: the earlier fully unrolled form -- 17 shuffles per pivot, two inlined copies,
-    // ~840 instructions each -- spent 36k cycles, 18 us, in its first call on i-cache misses).
-    auto phase1 = [&](int kb, double *wk) {
+    // phase 1 of block kb: LDL^T of the diagonal block, W_KK into wkk[buf] (write; a warp that
+    // runs it with write = false only keeps its SM sub-partition busy, see below)
+    auto phase1 = [&](int kb, double *wk, bool write) {
       const int k0 = kb * 8;
-      const int i = lane >> 2, q = lane & 3, ca = 2 * q, cb = ca + 1;
-      const int r = k0 + i;
-      double d0 = r >= k0 + ca ? M[r + (k0 + ca) * CB_LD] : M[(k0 + ca) + r * CB_LD];
-      double d1 = r >= k0 + cb ? M[r + (k0 + cb) * CB_LD] : M[(k0 + cb) + r * CB_LD];
-      double w0 = (i == ca) ? 1.0 : 0.0, w1 = (i == cb) ? 1.0 : 0.0;
-  #pragma unroll 1
+      const int i = lane & 7;
+      double d[8], w[8], g0[8], piv[8], sv[8];  // lane i: row i of the block and of W_KK
+  #pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = k0 + i, cc = k0 + j;
+        d[j] = r >= cc ? M[r + cc * CB_LD] : M[cc + r * CB_LD];
+        w[j] = (i == j) ? 1.0 : 0.0;
+        g0[j] = g0s[cc];
+      }
+      // the pivot chain only: shuffles, the reciprocal and FMAs (bookkeeping after the loop)
+      unsigned kinds = 0;
+  #pragma unroll
       for (int p = 0; p < 8; ++p) {
-        const bool odd = p & 1;
-        const double draw = __shfl_sync(0xffffffffu, odd ? d1 : d0, p * 4 + (p >> 1));   // D(p, p)
-        const double dip = __shfl_sync(0xffffffffu, odd ? d1 : d0, i * 4 + (p >> 1));    // D(i, p)
-        const double dp0 = __shfl_sync(0xffffffffu, d0, p * 4 + q), dp1 = __shfl_sync(0xffffffffu, d1, p * 4 + q);
-        const double wp0 = __shfl_sync(0xffffffffu, w0, p * 4 + q), wp1 = __shfl_sync(0xffffffffu, w1, p * 4 + q);
-        const double g0 = g0s[k0 + p];
-        unsigned kind = 0;
+        const double draw = __shfl_sync(0xffffffffu, d[p], p);
         double pv = draw;
-        if (!isfinite(draw)) { kind = 2; pv = 1.0; }
-        else if (dep_att && !(draw > CHOL_DEP * g0)) { kind = 1; pv = 1.0; }
-        else if (!(draw > CHOL_BREAK * g0)) { kind = 2; pv = 1.0; }
+        if (!isfinite(draw)) { kinds |= 2u << (2 * p); pv = 1.0; }
+        else if (dep_att && !(draw > CHOL_DEP * g0[p])) { kinds |= 1u << (2 * p); pv = 1.0; }
+        else if (!(draw > CHOL_BREAK * g0[p])) { kinds |= 2u << (2 * p); pv = 1.0; }
+        piv[p] = pv;
         const double pinv = fast_rcp(pv);
-        if (i > p && q == (p >> 1)) M[r + (k0 + p) * CB_LD] = odd ? d1 : d0;   // final S value L_ip d_p
-        const double l = (i > p) ? dip * pinv : 0.0;                            // L_ip
-        if (ca > p) d0 = fma(-l, dp0, d0);
-        if (cb > p) d1 = fma(-l, dp1, d1);
-        if (ca <= p) w0 = fma(-l, wp0, w0);
-        if (cb <= p) w1 = fma(-l, wp1, w1);
-        if (lane == 0) {   // pivot p's bookkeeping (uniform values)
-          const int kg = k0 + p;
-          // a numerically dependent column (pivot <= 1e-15 of its diagonal before any shift):
-          // reported as RQLP_FLAG_RANK_DEFICIENT whether or not the column is completed here
-          if (attempt == 0 && kg < n && !(draw > CHOL_DEP * g0) && !isnan(draw)) s_tiny = 1;
-          dpiv[kg] = pv;
-          dinv[kg] = pinv;
-          if (kg < n) {
-            if (dep_att) dep_att[kg] = kind == 1;
-            if (kind == 1) s_dep = 1;
-            if (kind == 2) s_fail = 1;
-          }
+        sv[p] = d[p];                                   // final S value L_ip d_p (i > p)
+        const double l = (i > p) ? d[p] * pinv : 0.0;  // L_ip (row i of the block)
+  #pragma unroll
+        for (int j = p + 1; j < 8; ++j) d[j] = fma(-l, __shfl_sync(0xffffffffu, d[j], p), d[j]);
+  #pragma unroll
+        for (int t = 0; t <= p; ++t) w[t] = fma(-l, __shfl_sync(0xffffffffu, w[t], p), w[t]);
+      }
+      if (!write) return;
+      if (lane < 8) {
+  #pragma unroll
+        for (int p = 0; p < 8; ++p)
+          if (i > p) M[(k0 + i) + (k0 + p) * CB_LD] = sv[p];
+        const int kg = k0 + i;  // lane i records pivot i
+        double pv = piv[0], dr = d[0];
+  #pragma unroll
+        for (int p = 1; p < 8; ++p) if (i == p) { pv = piv[p]; dr = d[p]; }
+        // a numerically dependent column (pivot <= 1e-15 of its diagonal before any shift):
+        // reported as RQLP_FLAG_RANK_DEFICIENT whether or not the column is completed here
+        if (attempt == 0 && kg < n && !(dr > CHOL_DEP * g0s[kg]) && !isnan(dr)) s_tiny = 1;
+        dpiv[kg] = pv;
+        dinv[kg] = fast_rcp(pv);
+        const unsigned kind = (kinds >> (2 * i)) & 3u;
+        if (kg < n) {
+          if (dep_att) dep_att[kg] = kind == 1;
+          if (kind == 1) s_dep = 1;
+          if (kind == 2) s_fail = 1;
         }
       }
-      wk[i * 8 + ca] = w0;
-      wk[i * 8 + cb] = w1;
-      if (ca < i) M[(k0 + ca) + r * CB_LD] = w0;   // W_{k0+i, k0+t} in the upper part
-      if (cb < i) M[(k0 + cb) + r * CB_LD] = w1;
+      if (lane < 8) {
+  #pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          wk[i * 8 + t] = w[t];
+          if (t < i) M[(k0 + t) + (k0 + i) * CB_LD] = w[t];  // W_{k0+i, k0+t} in the upper part
+        }
+      }
     };
     // debug (RQLP_ENGINE_TRACE): SM clock at the phases of every block of the first attempt
     auto stamp = [&](int kb, int ph) {
       if (trace && attempt == 0 && kb < 32) trace[kb * 4 + ph] = (unsigned long long)clock64();
     };
     if (tid == 0) stamp(31, 0);
-    if (warp == 0) phase1(0, wkk[0]);
+    // every warp runs block 0's phase 1 (only warp 0 writes).  Measured on this B200: a lone warp's
+    // latency-bound pivot chain ran ~5x slower while the other 15 warps were parked at
+    // __syncthreads (block 0: 35.8k cycles, 4.5k per pivot) than while they were busy (~0.4k per
+    // pivot in the loop below); redundant copies keep the sub-partitions busy (nothing parks).
+    phase1(0, wkk[0], warp == 0);
     if (tid == 0) stamp(31, 1);
 
     __syncthreads();
@@ -289,10 +301,13 @@ __global__ void __launch_bounds__(512, 1) chol_blk_kernel(int n, const double *G
         if (warp == 0) {
           tile(0);
           __syncwarp();
-          phase1(kb + 1, wkk[(kb + 1) & 1]);
+          phase1(kb + 1, wkk[(kb + 1) & 1], true);
           if (lane == 0) stamp(kb, 3);
         } else {
           for (int t = warp; t < n_s + n_w; t += nwarps - 1) tile(t);
+          // until warp 0's lookahead phase 1 is done: a redundant, non-writing copy of it (from
+          // whatever the diagonal block holds) instead of parking at the barrier (see above)
+          if (busy) phase1(kb + 1, nullptr, false);
         }
       }
       __syncthreads();
@@ -427,6 +442,19 @@ __global__ void add_shift_kernel(int c, double *G, int64_t ldg, double m, unsign
   }
 }
 
+// RQLP_CHOL_BUSY=1 (measurement switch): the trailing-update warps run a redundant phase 1 while
+// warp 0 runs the lookahead one, instead of parking at the barrier.  Measured: slower (C2's c = 110
+// blocked loop 29.0 -> 43.7 us -- the copies compete with warp 0 for issue), so off; only block 0's
+// phase 1, where all 15 other warps would otherwise park, runs redundantly.
+static int chol_busy() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RQLP_CHOL_BUSY");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *Gorig, int64_t ldo, double *R,
                      int64_t ldr, double *X, int64_t ldx, unsigned *fail_word, unsigned fail_bit,
                      const unsigned *cond, unsigned mask, int *dep = nullptr, unsigned dep_bit = 0, int near_id = 0,
@@ -436,7 +464,7 @@ void launch_chol_inv(Ctx &c, int n, const double *G, int64_t ldg, const double *
   chol_blk_kernel<<<1, 512, (size_t)((n + 7) & ~7) * CB_LD * 8, c.stream>>>(
       n, G, ldg, Gorig, ldo, R, ldr, X, ldx, fail_word, fail_bit, dep, dep_bit, c.dflags + FLAG_WORD, cond, mask,
       near_id, shift_m, c.dflags + COND_WORD, shift_bit, maxdev, nmaxdev, zero_cond,
-      c.trace ? c.trace + 8 * 4096 : nullptr);
+      c.trace ? c.trace + 8 * 4096 : nullptr, chol_busy());
   RQLP_LAUNCHED(c);
 }
 

@@ -25,7 +25,10 @@ lib.rqlp_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_in
 n = 16 * 4096
 buf = (ctypes.c_ulonglong * n)()
 assert lib.rqlp_debug_trace(buf, n) == 0
-t = np.array(buf[8 * 4096:8 * 4096 + 128], dtype=np.int64).reshape(32, 4)
+raw = np.array(buf[8 * 4096:8 * 4096 + 160], dtype=np.int64)
+t = raw[:128].reshape(32, 4)
+pv = raw[128:137]
+print("phase1(block 0) per pivot:", np.diff(pv).tolist(), " start offset", int(pv[0] - t[31, 0]), " end->stamp", int(t[31, 1] - pv[8]))
 nt = (c + 7) // 8
 print(f"chol_blk n={c}: phase1(block 0) {t[31, 1] - t[31, 0]} cycles")
 print(" kb   phase2  phase3  (warp0: tile0+phase1(kb+1))  block total")

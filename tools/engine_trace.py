@@ -30,3 +30,5 @@ d_upd = t[1:, 3] - t[1:, 2]
 d_pub = t[1:, 0] - t[:-1, 3]
 print(f"l={l} n={n}: per-step SM cycles  poll/exchange {np.median(d_poll):.0f}  reflector {np.median(d_refl):.0f}  "
       f"update {np.median(d_upd):.0f}  publish {np.median(d_pub):.0f}  total/step {np.median(np.diff(t[:, 0])):.0f}")
+d = np.diff(t[:, 0])
+print(f"   first steps (cycles): {d[:4].astype(int).tolist()}  last: {d[-3:].astype(int).tolist()}")
