@@ -82,6 +82,8 @@ struct EngineArgs {
   int *done;                // done[col] = 1 once pivoted (compaction of the non-pivot columns)
   int64_t *perm;
   int npoll;                 // warps that poll the exchange records (redundantly; warp 0 publishes p)
+  int w0free;                // warp 0 (the poller) takes no deferred column updates
+  int gtime;                 // debug trace: %globaltimer (ns) instead of clock64
 };
 
 // Exchange words: gpu-scope relaxed accesses (every word carries its step tag, so no ordering
@@ -151,6 +153,17 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
     int src = -1;
     if (a.pivot) src = c.i != 0x7fffffff ? c.i : -1;
     else if (jn < a.cols && jn % G == b) src = jn;
+    auto record = [&]() {
+      if (lane == 0 && (a.pivot || src >= 0)) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(a.pivot ? c.v : 0.0);
+        unsigned long long *rc = a.rec + ((int64_t)par * G + b) * 4;
+        st_x2(rc, pack((unsigned)(bits >> 32), tag), pack((unsigned)bits, tag));
+        st_x1(rc + 2, pack((unsigned)(a.pivot ? c.i : src), tag));
+      }
+    };
+    // the record first: the pollers' argmax does not wait for the column (the fetch spins on
+    // each row's tag, so the order of the words does not matter)
+    record();
     if (src >= 0) {
       const double *sp = colptr((src - b) / G);
       unsigned long long *dst = a.cand + ((int64_t)par * G + b) * (rows + 1) * 2;
@@ -166,12 +179,6 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
         const unsigned long long bits = (unsigned long long)__double_as_longlong(s2);
         st_x2(dst + 2 * (rows - jn), pack((unsigned)bits, tag), pack((unsigned)(bits >> 32), tag));
       }
-    }
-    if (lane == 0 && (a.pivot || src >= 0)) {
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(a.pivot ? c.v : 0.0);
-      unsigned long long *rc = a.rec + ((int64_t)par * G + b) * 4;
-      st_x2(rc, pack((unsigned)(bits >> 32), tag), pack((unsigned)bits, tag));
-      st_x1(rc + 2, pack((unsigned)(a.pivot ? c.i : src), tag));
     }
   };
 
@@ -199,6 +206,15 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
   __syncthreads();
   if (GRID && warp == 0) publish(0, cta_best(0));
 
+  // per-CTA debug stamps: [step 20..59][CTA][poll start, poll done, fetch done, record out]
+  auto cstamp = [&](int jj, int k) {
+    if (a.trace && GRID && threadIdx.x == 0 && jj >= 20 && jj < 60 && b < 148) {
+      unsigned long long t;
+      if (a.gtime) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      else t = (unsigned long long)clock64();
+      a.trace[8192 + ((int64_t)(jj - 20) * 148 + b) * 4 + k] = t;
+    }
+  };
   for (int j = 0; j < a.steps; ++j) {
     const int par = j & 1;
     auto stamp = [&](int ph) {
@@ -207,6 +223,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       }
     };
     stamp(0);
+    cstamp(j, 0);
     const int len = rows - j;
     const double *cp;  // rows j.. of the pivot column
     int p;
@@ -248,6 +265,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
         }
         if (warp == 0 && lane == 0) s_p = c.i;
       }
+      cstamp(j, 1);
       __syncthreads();
       p = s_p;
       const unsigned long long *src = a.cand + ((int64_t)par * G + (p % G)) * (rows + 1) * 2;
@@ -267,6 +285,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
       cp = colptr(p) + j;
     }
     stamp(1);
+    cstamp(j, 2);
 
     // ---- reflector (xLARFG), recomputed by every warp from the same values -> identical bits
     //      (grid: ||rows j+1..||^2 comes with the candidate, summed once by its publisher)
@@ -464,6 +483,13 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
           const unsigned tag = (a.epoch << 16) | ((unsigned)jn + 1u);
           double *cab = colptr(lbest);
           unsigned long long *dst = a.cand + ((int64_t)par2 * G + b) * (rows + 1) * 2;
+          if (lane == 0) {   // the record first (see publish)
+            const unsigned long long vb = (unsigned long long)__double_as_longlong(cb.v);
+            unsigned long long *rc = a.rec + ((int64_t)par2 * G + b) * 4;
+            st_x2(rc, pack((unsigned)(vb >> 32), tag), pack((unsigned)vb, tag));
+            st_x1(rc + 2, pack((unsigned)cb.i, tag));
+          }
+          cstamp(jn, 3);
           double s2 = 0.0;
           for (int r = jn + lane; r < rows; r += 32) {
             const double v = fma(-wsb, cp[r - j], cab[r]);
@@ -476,10 +502,6 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
           if (lane == 0) {
             const unsigned long long sb = (unsigned long long)__double_as_longlong(s2);
             st_x2(dst + 2 * (rows - jn), pack((unsigned)sb, tag), pack((unsigned)(sb >> 32), tag));
-            const unsigned long long vb = (unsigned long long)__double_as_longlong(cb.v);
-            unsigned long long *rc = a.rec + ((int64_t)par2 * G + b) * 4;
-            st_x2(rc, pack((unsigned)(vb >> 32), tag), pack((unsigned)vb, tag));
-            st_x1(rc + 2, pack((unsigned)cb.i, tag));
           }
         } else {
           if (wsb != 0.0) finish(lbest, lane, 32);
@@ -487,9 +509,12 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : 256) : 1024, 1) hh_engin
           if (j + 1 < a.steps) publish(j + 1, cb);
         }
       }
-      if (tau != 0.0) {
+      if (tau != 0.0 && !(a.w0free && warp == 0)) {
+        // w0free: warp 0 polls the next step's records while warps 1.. finish its columns (measured
+        // C2-shaped 110 x 4096: 565 -> 521 us; 272 x 8192: 1870 -> 1649 us)
         const int g8 = lane >> 3, l8 = lane & 7;
-        for (int li = warp * 4 + g8; li < nown; li += wpb * 4)
+        const int w = a.w0free ? warp - 1 : warp, nw = a.w0free ? wpb - 1 : wpb;
+        for (int li = w * 4 + g8; li < nown; li += nw * 4)
           if (li != lbest && b + li * G != p && !done_l[li]) finish(li, l8, 8);
       }
     } else if (GRID && warp == 0 && j + 1 < a.steps) {
@@ -760,6 +785,14 @@ void hh_factor(Ctx &c, HHScratch &s, int64_t rows, int64_t cols, double *M, int6
       np = e ? std::max(1, atoi(e)) : 1;
     }
     a.npoll = np;
+    static int w0f = -1;   // RQLP_ENGINE_W0FREE (measurement switch)
+    if (w0f < 0) {
+      const char *e = getenv("RQLP_ENGINE_W0FREE");
+      w0f = e ? atoi(e) : 1;
+    }
+    a.w0free = w0f;
+    const char *tr = getenv("RQLP_ENGINE_TRACE");
+    a.gtime = tr && tr[0] == '2';
   }
   auto smem_for = [&](int64_t owned, bool cached) {
     const int64_t rs = round_up(rows, 2), op = round_up(owned, 2);
