@@ -33,6 +33,19 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
 namespace {
 
 constexpr int BM = 128, BK = 24, STAGES = 4, NCONS = 8;
+// CTAs per SM of the plain (non-||A||^2) kernel of width bn = 64: 2 when the launch has many tiles
+// or much work per tile (measured, C4-sized operands: the 64-wide A-passes 34.6 -> 36.2 TFLOP/s,
+// m x 64 times 64 x 64 133 -> 93 us; a single-tile Gram or few short tiles lose with 3 stages);
+// else 1.  RQLP_GEMM_OCC2=0 keeps 1 (measurement switch).
+int gemm_occ(int bn, bool fro, int64_t tiles = 1 << 30, int64_t ktiles = 1 << 30) {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("RQLP_GEMM_OCC2");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!on || bn != 64 || fro) return 1;
+  return (tiles >= 296 || tiles * ktiles >= 40000) ? 2 : 1;
+}
 // the ||A||^2 warp makes 9 warps: 3 on one SM sub-partition caps the registers at 168 per thread,
 // which spills the accumulators for BN > 96 -- those passes use a separate ||A||^2 pass
 constexpr int FRO_MAX_BN = 96;
@@ -79,8 +92,10 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 
 // MODE 0 = NN, 1 = TN.  Output element (i, j) of the (M x N) product goes to
 //   part (split-K slice, M x N contiguous)  or  C[i + j ldc]  or (trans) C[j + i ldc].
-template <int BN, int MODE, bool FRO>
-__global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
+// OCC = 2 (BN = 64 only): two CTAs per SM (3-stage rings, <= 128 registers): 16 warps hide the
+// DMMA chains of the narrow 32 x 32 warp tiles better than 8 (measured in DESIGN.md §5).
+template <int BN, int MODE, bool FRO, int OCC = 1>
+__global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, OCC)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
                     int ktiles_total, int ktiles_per_split, double *__restrict__ C, int64_t ldc, int trans,
                     double *__restrict__ part, const unsigned *cond, unsigned cond_mask, int tri, int bal_units,
@@ -90,13 +105,14 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
   // the diagonal do nothing (a Gram; consumers read the upper triangle).  tri == 2: the B operand
   // is upper triangular -- k-tiles at or beyond n0 + BN contribute nothing (Y R^-1).
   if (tri == 1 && (int)(blockIdx.y * BM) >= (int)(blockIdx.x * BN) + BN) return;
+  constexpr int NST = OCC == 2 ? 3 : STAGES;
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
   constexpr int B_BYTES = BN * BK * 8;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr int NB = BN / 16;  // 8-col fragments per warp (warp tile 32 x BN/2)
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty = full + STAGES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * STAGE_BYTES);
+  uint64_t *empty = full + NST;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // balanced split (bal_units > 0, tri == 0): the (tile, k-tile) units in tile-major order are
@@ -132,7 +148,7 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCONS + (FRO ? 1 : 0));
     }
@@ -140,9 +156,9 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
   }
   __syncthreads();
 
-  // ---------------- producer role (thread 0 of warp 0): TMA slabs STAGES-1 iterations ahead
+  // ---------------- producer role (thread 0 of warp 0): TMA slabs NST-1 iterations ahead
   auto issue = [&](int it) {
-    const int s = it % STAGES;
+    const int s = it % NST;
     unsigned char *sa = smem + s * STAGE_BYTES;
     unsigned char *sb = sa + A_BYTES;
     int tm0, tn0, kk;
@@ -155,7 +171,7 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapB) : "memory");
-    for (int it = 0; it < STAGES - 1 && it < nkt; ++it) issue(it);
+    for (int it = 0; it < NST - 1 && it < nkt; ++it) issue(it);
   }
 
   // ---------------- ||A||_F^2 fused into the NN pass (eq. (3); FRO, MODE 0): a 9th
@@ -169,8 +185,8 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
     double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
     const bool fro_on = bal || n0 == 0;
     for (int it = 0; it < nkt; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
+      const int s = it % NST;
+      mbar_wait(&full[s], (it / NST) & 1);
       // balanced runs: count the unit if its tile is in output column tile 0
       if (fro_on && (!bal || ((u0 + it) / ktiles_total) % ntn == 0)) {
         const double *sa = reinterpret_cast<const double *>(smem + s * STAGE_BYTES);
@@ -204,13 +220,13 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, 1)
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int it = 0; it < nkt; ++it) {
-    const int s = it % STAGES;
-    if (threadIdx.x == 0 && it + STAGES - 1 < nkt) {
+    const int s = it % NST;
+    if (threadIdx.x == 0 && it + NST - 1 < nkt) {
       // refill the slot consumed at iteration it-1 once every warp has released it
-      if (it >= 1) mbar_wait(&empty[(it - 1) % STAGES], ((it - 1) / STAGES) & 1);
-      issue(it + STAGES - 1);
+      if (it >= 1) mbar_wait(&empty[(it - 1) % NST], ((it - 1) / NST) & 1);
+      issue(it + NST - 1);
     }
-    mbar_wait(&full[s], (it / STAGES) & 1);
+    mbar_wait(&full[s], (it / NST) & 1);
     const double *sa = reinterpret_cast<const double *>(smem + s * STAGE_BYTES);
     const double *sb = reinterpret_cast<const double *>(smem + s * STAGE_BYTES + A_BYTES);
 #pragma unroll
@@ -493,8 +509,10 @@ ColSplit choose_colsplit(int64_t cc, int64_t ktiles) {
 //                                      + (S > 1) * (2 S M N 8 bytes / HBM + reduce launch)
 // with T = tiles * S CTAs (1 CTA per SM), t_ktile = 128 BN 24 2 flop / (DMMA peak per SM).
 int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int64_t out_elems, int bn,
-                  double *t_out = nullptr) {
-  const double t_ktile = 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);   // s
+                  double *t_out = nullptr, int occ = 1) {
+  // occ CTAs per SM: num_sms x occ concurrent CTAs, each at 1/occ of the SM's DMMA rate
+  num_sms *= occ;
+  const double t_ktile = occ * 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);   // s
   const double hbm = 6.0e12;                                           // B/s
   int best = 1;
   double best_t = 1e300;
@@ -519,16 +537,19 @@ int choose_splits(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap
 // the run length when its modelled time beats the split-K time t_split (and the slots fit), else 0.
 struct BalPlan {
   int units = 0, maxc = 0;
+  int occ = 1;   // CTAs per SM the split models assumed (gemm_occ): the launch uses the same
 };
-BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int bn, double t_split) {
+BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t partial_cap_elems, int bn, double t_split,
+                        int occ = 1) {
   BalPlan p;
+  num_sms *= occ;
   const int64_t total = tiles * ktiles;
   if (tiles >= num_sms || total < 4 * (int64_t)num_sms || total >= (1ll << 31)) return p;
   const int64_t U = ceil_div(total, num_sms);
   int64_t maxc = 0;
   for (int64_t t = 0; t < tiles; ++t) maxc = std::max<int64_t>(maxc, ((t + 1) * ktiles - 1) / U - (t * ktiles) / U + 1);
   if ((size_t)(tiles * maxc * BM * bn) > partial_cap_elems) return p;
-  const double t_ktile = 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);
+  const double t_ktile = occ * 128.0 * bn * BK * 2.0 / (37.0e12 / 148.0);
   const double hbm = 6.0e12;
   const double t = (double)(U + 3) * t_ktile + 2.0 * (double)(tiles + num_sms) * BM * bn * 8.0 / hbm + 4e-6;
   if (t < 0.9 * t_split) {  // measured: a 5% gain at C2 (c = 110), a loss at c <= 40
@@ -538,13 +559,14 @@ BalPlan choose_balanced(int64_t tiles, int64_t ktiles, int num_sms, size_t parti
   return p;
 }
 
-template <int BN, int MODE, bool FRO>
-void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+template <int BN, int MODE, bool FRO, int OCC>
+void launch_bn_o(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
                  int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
                  const FroSpec *fro, double alpha, double beta) {
+  constexpr int NST = OCC == 2 ? 3 : STAGES;
   constexpr int A_BYTES = MODE == 0 ? A_TILE_BYTES_NN : A_TILE_BYTES_TN;
-  constexpr int SMEM = STAGES * (A_BYTES + BN * BK * 8) + 2 * STAGES * 8;
-  smem_attr((const void *)gemm_tma_kernel<BN, MODE, FRO>, SMEM);
+  constexpr int SMEM = NST * (A_BYTES + BN * BK * 8) + 2 * NST * 8;
+  smem_attr((const void *)gemm_tma_kernel<BN, MODE, FRO, OCC>, SMEM);
   double *fslots = fro ? fro->slots : nullptr;
   auto fro_finish = [&](int64_t nctas) {
     if (!fro) return;
@@ -555,7 +577,7 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
     const int ntn = (int)ceil_div(N, BN);
     const int64_t total = (int64_t)ktiles * ntn * ceil_div(M, BM);
     const unsigned ctas = (unsigned)ceil_div(total, bp.units);
-    gemm_tma_kernel<BN, MODE, FRO><<<ctas, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
+    gemm_tma_kernel<BN, MODE, FRO, OCC><<<ctas, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, 0, C, ldc, trans ? 1 : 0,
                                                                      part, cond, mask, 0, bp.units, ntn, bp.maxc,
                                                                      fslots, alpha, beta);
     RQLP_LAUNCHED(c);
@@ -569,12 +591,26 @@ void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, in
   int kps = (int)ceil_div(ktiles, S);
   S = (int)ceil_div(ktiles, kps);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)S);
-  gemm_tma_kernel<BN, MODE, FRO><<<grid, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
+  gemm_tma_kernel<BN, MODE, FRO, OCC><<<grid, (NCONS + (FRO ? 1 : 0)) * 32, SMEM, c.stream>>>(ma, mb, M, N, ktiles, kps, C, ldc,
                                                                        trans ? 1 : 0, S > 1 ? part : nullptr, cond,
                                                                        mask, tri, 0, 1, 1, fslots, alpha, beta);
   RQLP_LAUNCHED(c);
   fro_finish((int64_t)grid.x * grid.y * grid.z);
   if (S > 1) launch_reduce(c, M, N, S, part, alpha, beta, C, ldc, trans, cond, mask);
+}
+
+template <int BN, int MODE, bool FRO>
+void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
+                 int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
+                 const FroSpec *fro, double alpha, double beta) {
+  if constexpr (BN == 64 && !FRO) {
+    if (bp.occ == 2) {
+      launch_bn_o<64, MODE, false, 2>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha,
+                                      beta);
+      return;
+    }
+  }
+  launch_bn_o<BN, MODE, FRO, 1>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha, beta);
 }
 
 template <int BN, int MODE>
@@ -635,10 +671,13 @@ size_t gemm_tma_partials_needed(int64_t m, int64_t cc, int64_t k, int num_sms) {
   auto need = [&](int64_t M, int64_t cols, int64_t ktiles, int bn) {
     int64_t tiles = ceil_div(M, BM) * ceil_div(cols, bn);
     double ts = 0.0;
-    int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cols, bn, &ts);
-    if (S > 1) best = std::max(best, (size_t)S * M * cols);
-    BalPlan bp = choose_balanced(tiles, ktiles, num_sms, (size_t)1 << 62, bn, ts);
-    if (bp.units > 0) best = std::max(best, (size_t)tiles * bp.maxc * BM * bn);
+    const int occ = gemm_occ(bn, false, tiles, ktiles);   // the partials of both occupancies (upper bound)
+    for (int o = 1; o <= occ; ++o) {
+      int S = choose_splits(tiles, ktiles, num_sms, (size_t)1 << 62, M * cols, bn, &ts, o);
+      if (S > 1) best = std::max(best, (size_t)S * M * cols);
+      BalPlan bp = choose_balanced(tiles, ktiles, num_sms, (size_t)1 << 62, bn, ts, o);
+      if (bp.units > 0) best = std::max(best, (size_t)tiles * bp.maxc * BM * bn);
+    }
   };
   for (int mode = 0; mode < 2; ++mode) {
     int64_t M = mode == 0 ? m : k, K = mode == 0 ? k : m;
@@ -721,10 +760,12 @@ bool gemm_nn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, i
   int64_t ktiles = ceil_div(k, BK);
   int64_t tiles = ceil_div(m, BM) * ceil_div(cc, bn);
   double ts = 0.0;
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn, &ts);
+  const int occ = gemm_occ(bn, fro != nullptr, tiles, ktiles);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, m * cc, bn, &ts, occ);
   BalPlan bp;
   if (tri == 0 && partials && !balanced_disabled())
-    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
+    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts, occ);
+  bp.occ = occ;
   if (fro) {   // the slots needed by this launch configuration must fit
     const int64_t ctas = bp.units > 0 ? ceil_div(tiles * ktiles, bp.units)
                                       : tiles * ceil_div(ktiles, ceil_div(ktiles, S));
@@ -774,10 +815,12 @@ bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, i
       for (int64_t nt = 0; nt < ceil_div(cc, bn); ++nt) tiles += (mt * BM < nt * bn + bn) ? 1 : 0;
   }
   double ts = 0.0;
-  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn, &ts);
+  const int occ = gemm_occ(bn, false, tiles, ktiles);
+  int S = choose_splits(tiles, ktiles, c.num_sms, partials ? partial_elems : 0, k * cc, bn, &ts, occ);
   BalPlan bp;
   if (tri == 0 && partials && !balanced_disabled())
-    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts);
+    bp = choose_balanced(tiles, ktiles, c.num_sms, partial_elems, bn, ts, occ);
+  bp.occ = occ;
   dispatch<1>(c, bn, ma, mb, (int)k, (int)cc, (int)ktiles, S, Z, ldz, trans_out, partials, cond, cond_mask, tri, bp,
               nullptr, alpha, beta);
   return true;
