@@ -13,9 +13,10 @@
 // Host-resident A of rqlp_factorize: copied in row panels on a copy stream while the sketch pass
 // consumes the panels that have landed (Y = AΩ is row-separable).
 struct HostFeed {
-  const double *hA = nullptr;
+  const double *hA = nullptr;   // host A fed in row panels (null: A is on the device)
   int64_t hlda = 0;
   int64_t panel_rows = 0;
+  double *hQ = nullptr, *hP = nullptr;   // BRQLP: pinned host Q / P, streamed out block by block
 };
 
 struct rqlp_handle_s {
@@ -62,6 +63,7 @@ struct rqlp_handle_s {
   const HostFeed *feed = nullptr;  // set by rqlp_factorize for its host A (one call at a time)
   cudaStream_t cstream = nullptr;  // copy stream of the host feed and its events
   std::vector<cudaEvent_t> cev;
+  std::vector<cudaEvent_t> oev;   // BRQLP host outputs: one per block + the join
   cudaStream_t side = nullptr;  // Ctx::branch() stream and its fork/join events
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
@@ -238,6 +240,8 @@ std::string make_key(rqlp_handle_t h, const char *tag, std::initializer_list<int
     put(&h->feed->hA, sizeof h->feed->hA);
     put(&h->feed->hlda, sizeof h->feed->hlda);
     put(&h->feed->panel_rows, sizeof h->feed->panel_rows);
+    put(&h->feed->hQ, sizeof h->feed->hQ);
+    put(&h->feed->hP, sizeof h->feed->hP);
   }
   return k;
 }
@@ -373,7 +377,7 @@ int check_common(int64_t m, int64_t n, int k, int p, int q) {
 void sketch_pass(Ctx &c, rqlp_handle_t h, const Plan &P, int64_t m, int64_t cols, int64_t n, const double *A,
                  int64_t lda, const double *X, int64_t ldx, double *Y, int64_t ldy) {
   const HostFeed *f = h->feed;
-  if (!f) {
+  if (!f || !f->hA) {
     gemm_nn_fro(c, m, cols, n, A, lda, X, ldx, Y, ldy, P.part, P.part_elems, FroSpec{P.fro_slots, P.fro_cap, c.dind});
     return;
   }
@@ -516,6 +520,15 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
   const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
+  const bool out = h->feed && (h->feed->hQ || h->feed->hP) && !ar;
+  if (out) {
+    if (!h->cstream) RQLP_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    while ((int64_t)h->oev.size() < h_blocks + 1) {
+      cudaEvent_t e;
+      RQLP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->oev.push_back(e);
+    }
+  }
   // Alg.3 l.4-5: V_j = qr(Y_j), then V_j <- qr(V_j - V_<j (V_<j^T V_j)) (eq. (18)), the latter
   // applied twice ("twice is enough", reading R28: identical in exact arithmetic when V_j has a
   // component outside span(V_<j) -- the second projection removes nothing -- and the only way to
@@ -636,7 +649,23 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     // l.9: Q_j = V_j Q_B
     gemm_nn(c, m, bj, bj, Vj, ldm, P.QB, P.tail.ldl, Q + c0 * ldq, ldq, P.part, P.part_elems);
     c.mark("block_tail");
+    if (out) {
+      // host outputs (rqlp_factorize): Q_j and P_j go out on the copy stream while the next
+      // blocks run (part of the captured work; joined below)
+      RQLP_CUDA(cudaEventRecord(h->oev[j], c.stream));
+      RQLP_CUDA(cudaStreamWaitEvent(h->cstream, h->oev[j], 0));
+      if (h->feed->hQ)
+        RQLP_CUDA(cudaMemcpy2DAsync(h->feed->hQ + c0 * m, m * 8, Q + c0 * ldq, ldq * 8, m * 8, bj,
+                                    cudaMemcpyDeviceToHost, h->cstream));
+      if (h->feed->hP)
+        RQLP_CUDA(cudaMemcpy2DAsync(h->feed->hP + c0 * n, n * 8, Pout + c0 * ldp, ldp * 8, n * 8, bj,
+                                    cudaMemcpyDeviceToHost, h->cstream));
+    }
     if (stop) break;
+  }
+  if (out) {   // join the copy stream
+    RQLP_CUDA(cudaEventRecord(h->oev[h_blocks], h->cstream));
+    RQLP_CUDA(cudaStreamWaitEvent(c.stream, h->oev[h_blocks], 0));
   }
   if (!ar) fro2_accumulate(c, l, n, B, LL, P.fro_slots, c.dind + 1, true);   // sum_j ||B_j||_F^2 (deflated B_j)
   if (h->dbgV) launch_copy(c, m, l, P.V, ldm, h->dbgV, h->ldV, false);
@@ -795,6 +824,7 @@ int rqlp_destroy(rqlp_handle_t h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->cstream) cudaStreamDestroy(h->cstream);
   for (auto ev : h->cev) cudaEventDestroy(ev);
+  for (auto ev : h->oev) cudaEventDestroy(ev);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own) cudaFree(h->own);
@@ -1010,6 +1040,15 @@ static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int
       feed.panel_rows = round_up(std::max(min_rows, ceil_div(m, 8)), 128);
       h->feed = &feed;
     }
+    // BRQLP with pinned host Q / P: each block's columns are copied out as soon as they are final
+    bool streamQ = false, streamP = false;
+    if (variant == RQLP_VARIANT_BRQLP) {
+      streamQ = !dQ && is_pinned_host_ptr(Q);
+      streamP = !dP && is_pinned_host_ptr(P);
+      if (streamQ) feed.hQ = Q;
+      if (streamP) feed.hP = P;
+      if (streamQ || streamP) h->feed = &feed;
+    }
     int r;
     try {
       if (variant == RQLP_VARIANT_BRQLP)
@@ -1024,9 +1063,9 @@ static int factorize_any(rqlp_handle_t h, int variant, int64_t m, int64_t n, int
     h->feed = nullptr;
     if (r) return r;
     if (t_is_upper) *t_is_upper = (variant == RQLP_VARIANT_ERQLP && d % 2 == 0) ? 1 : 0;
-    if (!dQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dQ && !streamQ) RQLP_CUDA(cudaMemcpyAsync(Q, Qd, (size_t)m * l * 8, cudaMemcpyDeviceToHost, h->stream));
     if (!dT) RQLP_CUDA(cudaMemcpyAsync(T, Td, (size_t)l * l * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (!dP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (!dP && !streamP) RQLP_CUDA(cudaMemcpyAsync(P, Pd, (size_t)n * l * 8, cudaMemcpyDeviceToHost, h->stream));
     RQLP_CUDA(cudaStreamSynchronize(h->stream));
     return RQLP_OK;
   }, true);

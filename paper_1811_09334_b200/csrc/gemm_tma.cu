@@ -33,17 +33,18 @@ void gemm_generic_ex(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, 
 namespace {
 
 constexpr int BM = 128, BK = 24, STAGES = 4, NCONS = 8;
-// CTAs per SM of the plain (non-||A||^2) kernel of width bn = 64: 2 when the launch has many tiles
-// or much work per tile (measured, C4-sized operands: the 64-wide A-passes 34.6 -> 36.2 TFLOP/s,
-// m x 64 times 64 x 64 133 -> 93 us; a single-tile Gram or few short tiles lose with 3 stages);
-// else 1.  RQLP_GEMM_OCC2=0 keeps 1 (measurement switch).
+// CTAs per SM of the plain (non-||A||^2) kernel of width bn = 32..64: 2 when the launch has many
+// tiles or much work per tile (measured, C4-sized operands: the 64-wide A-passes 34.6 -> 36.2
+// TFLOP/s, 48-wide 34.6 -> 35.9, 32-wide 30.4 -> 33.8, m x 64 times 64 x 64 133 -> 93 us; a
+// single-tile Gram or few short tiles lose with 3 stages); else 1.  RQLP_GEMM_OCC2=w: widths <= w
+// (0: none; measurement switch).
 int gemm_occ(int bn, bool fro, int64_t tiles = 1 << 30, int64_t ktiles = 1 << 30) {
   static int on = -1;
   if (on < 0) {
     const char *e = getenv("RQLP_GEMM_OCC2");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = e ? atoi(e) : 64;   // the widest tile width that runs two CTAs per SM (0: none)
   }
-  if (!on || bn != 64 || fro) return 1;
+  if (!on || bn > on || bn < 32 || fro) return 1;   // (16: memory-bound, the TN pass loses 5.2 -> 5.7 ms)
   return (tiles >= 296 || tiles * ktiles >= 40000) ? 2 : 1;
 }
 // the ||A||^2 warp makes 9 warps: 3 on one SM sub-partition caps the registers at 168 per thread,
@@ -603,9 +604,9 @@ template <int BN, int MODE, bool FRO>
 void launch_bn_t(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, int M, int N, int ktiles, int S, double *C,
                  int64_t ldc, bool trans, double *part, const unsigned *cond, unsigned mask, int tri, BalPlan bp,
                  const FroSpec *fro, double alpha, double beta) {
-  if constexpr (BN == 64 && !FRO) {
+  if constexpr (BN <= 64 && !FRO) {
     if (bp.occ == 2) {
-      launch_bn_o<64, MODE, false, 2>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha,
+      launch_bn_o<BN, MODE, false, 2>(c, ma, mb, M, N, ktiles, S, C, ldc, trans, part, cond, mask, tri, bp, fro, alpha,
                                       beta);
       return;
     }

@@ -303,6 +303,28 @@ def test_host_pointer_entry_points(rq, orc):
     assert tu
 
 
+@pytest.mark.parametrize("pin_a", [True, False])
+def test_brqlp_host_outputs_streamed(rq, pin_a):
+    """BRQLP through rqlp_factorize with pinned host Q/P: each block's Q_j, P_j is copied out on the
+    copy stream while the later blocks run; the result equals the device path bit for bit (ragged
+    last block; pinned A fed in row panels, or pageable A copied up front), also on a graph replay."""
+    A = _rand_svd(1500, 700, np.exp(-np.arange(1, 701.0) / 40), 77)
+    g = rq.factorize(_cm(A), 40, 10, q=1, b=16, seed=5)
+    At = torch.from_numpy(np.ascontiguousarray(A.T))
+    if pin_a:
+        At = At.pin_memory()
+    At = At.t()
+    out = tuple(torch.empty(c, r, dtype=torch.float64, pin_memory=True).t() for r, c in ((1500, 50), (50, 50), (700, 50)))
+    h = rq.Handle()
+    for _ in range(2):   # the second call replays the captured graph
+        for t in out:
+            t.fill_(np.nan)
+        Q, T, P, _ = rq.factorize_host(At, 40, 10, q=1, b=16, seed=5, handle=h, out=out)
+        np.testing.assert_array_equal(Q.numpy(), _np(g["Q"]))
+        np.testing.assert_array_equal(T.numpy(), _np(g["T"]))
+        np.testing.assert_array_equal(P.numpy(), _np(g["P"]))
+
+
 def test_deterministic_reruns(rq):
     """Bitwise-identical results across reruns (fixed-order reductions, no atomics in sums)."""
     A = _cm(_rand_svd(1031, 1030, np.exp(-np.arange(1, 1031.0) / 50), 2))
