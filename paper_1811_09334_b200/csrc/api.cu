@@ -469,6 +469,14 @@ int run_rqlp(rqlp_handle_t h, int64_t m, int64_t n, int k, int p, int q, int d, 
 }
 
 // ---- BRQLP -------------------------------------------------------------------------------
+static bool fro_late_off() {   // RQLP_FRO_LATE=0: ||A||_F^2 always in the sketch (measurement switch)
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RQLP_FRO_LATE");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
 // Auto-rank mode of the block loop (NEXT-1): per-block sketches, and after
 // each block the eq. (3) indicator ||A||_F^2 - sum_j ||B_j||_F^2 is read back; the loop stops once
 // it is <= (eps ||A||_F)^2 (reading R25).
@@ -510,15 +518,22 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   launch_omega(c, n, l, 0, seed, P.Om, ldn);                                            // l.1
   c.mark("omega");
   const FroSpec fro{P.fro_slots, P.fro_cap, c.dind};
+  const int64_t h_blocks = ceil_div(l, b);
+  // ||A||_F^2 (eq. (3)) rides on an A-pass that reads A anyway.  Normally the sketch; when the last
+  // block is narrow (C4: 16 columns) and has a power step, its Y = A W pass instead: that pass is
+  // HBM-bound, so the extra warp squaring the staged A tiles costs nothing there, while in the
+  // compute-bound sketch it cost ~3 ms (C4).  Only BRQLP's final indicator reads it.
+  const int64_t b_last = l - (h_blocks - 1) * b;
+  const bool fro_late = !ar && q > 0 && b_last <= 32 && !(h->feed && h->feed->hA) && !fro_late_off();
   if (!ar) {
     // l.3 all Y_j = AΩ_j in one pass, with ||A||_F^2 (eq. (3)) from the same A tiles
-    sketch_pass(c, h, P, m, l, n, A, lda, P.Om, ldn, P.Y, ldm);
-    allreduce_sum(c, c.dind, 1);   // row shards: ||A||^2 is the sum over ranks (B_j is replicated)
+    if (fro_late) gemm_nn(c, m, l, n, A, lda, P.Om, ldn, P.Y, ldm, P.part, P.part_elems);
+    else sketch_pass(c, h, P, m, l, n, A, lda, P.Om, ldn, P.Y, ldm);
+    if (!fro_late) allreduce_sum(c, c.dind, 1);   // row shards: ||A||^2 is the sum over ranks (B_j is replicated)
     c.mark("pass_sketch");
     if (h->dbgY) launch_copy(c, m, l, P.Y, ldm, h->dbgY, h->ldY, false);
   }
   launch_fill(c, l, l, L, ldl, 0.0, 0.0);
-  const int64_t h_blocks = ceil_div(l, b);
   double *B = P.B;  // B_<j rows accumulate here (l x n, ld LL)
   const bool out = h->feed && (h->feed->hQ || h->feed->hP) && !ar;
   if (out) {
@@ -601,7 +616,12 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
         orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
         if (h->dbgW) launch_copy(c, n, bj, P.W, ldn, h->dbgW + (it * l + c0) * h->ldW, h->ldW, false);
         c.mark("b_other");
-        gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
+        if (fro_late && j == h_blocks - 1 && it == 0) {   // Y = A W, with ||A||_F^2 (see above)
+          gemm_nn_fro(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems, fro);
+          allreduce_sum(c, c.dind, 1);
+        } else {
+          gemm_nn(c, m, bj, n, A, lda, P.W, ldn, P.Y + c0 * ldm, ldm, P.part, P.part_elems); // Y = A W
+        }
         c.mark("pass_block_AW");
         if (c0 > 0) {
           gemm_nn_ab(c, c0, bj, n, 1.0, B, LL, P.W, ldn, 0.0, P.D, LL, P.part, P.part_elems);    // D = B_<j W
