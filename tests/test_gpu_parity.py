@@ -48,8 +48,12 @@ def test_omega_bit_exact(rq, orc, n, l, seed):
 
 # (2000, 3000, 40), (4100, 4100, 110), (2500, 2600, 200): fewer output tiles than SMs and many
 # k-tiles -> the balanced split (equal runs of (tile, k-tile) units per CTA, ragged at both ends)
+# (40000, 300, 64), (38001, 1000, 48), (37900, 70, 33): >= 296 output tiles of width 32..64 -> two
+# CTAs per SM (3-stage rings), ragged rows / columns; (6000, 21000, 64): few tiles, many k-tiles ->
+# the two-CTA split-K / balanced split
 @pytest.mark.parametrize("m,k,c", [(1000, 800, 25), (1031, 1030, 110), (4133, 1029, 138), (517, 93, 17), (64, 64, 64),
-                                   (3, 5, 2), (2000, 3000, 40), (4100, 4100, 110), (2500, 2600, 200)])
+                                   (3, 5, 2), (2000, 3000, 40), (4100, 4100, 110), (2500, 2600, 200),
+                                   (40000, 300, 64), (38001, 1000, 48), (37900, 70, 33), (6000, 21000, 64)])
 def test_gemm_nn_parity(rq, orc, m, k, c):
     rng = np.random.default_rng(m + k + c)
     A, X = rng.standard_normal((m, k)), rng.standard_normal((k, c))
@@ -61,7 +65,8 @@ def test_gemm_nn_parity(rq, orc, m, k, c):
 
 @pytest.mark.parametrize("m,k,c,trans", [(1000, 800, 25, True), (1031, 1030, 110, False), (4133, 1029, 138, True),
                                          (517, 93, 17, False), (5, 3, 2, True), (3000, 2000, 40, True),
-                                         (4100, 4100, 110, False), (4100, 4100, 110, True), (2600, 2500, 200, False)])
+                                         (4100, 4100, 110, False), (4100, 4100, 110, True), (2600, 2500, 200, False),
+                                         (70001, 4000, 48, True), (64000, 2000, 64, False), (50000, 300, 64, True)])
 def test_gemm_tn_parity(rq, orc, m, k, c, trans):
     rng = np.random.default_rng(m * 3 + k + c)
     A, V = rng.standard_normal((m, k)), rng.standard_normal((m, c))
