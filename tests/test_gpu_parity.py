@@ -131,9 +131,11 @@ def test_orth_rescue(rq, orc, spec, m, c):
         np.testing.assert_allclose(np.abs(np.diag(R)[:k]), np.abs(np.diag(Ro)[:k]), rtol=1e-8)
 
 
-# (30, 17), (25, 25), (32, 32), (32, 7), (5, 32), (1, 1), (31, 29): the one-warp kernel (<= 32 x 32)
+# (30, 17), (25, 25), (32, 32), (32, 7), (5, 32), (1, 1), (31, 29): the one-warp kernel (<= 32 x 32);
+# (600, 8000), (460, 9001): columns in global memory (too many rows x columns per CTA for shared
+# memory) with the lazy panel updates: full panels, and a partial last panel (460 = 57 x 8 + 4)
 @pytest.mark.parametrize("rows,cols", [(25, 800), (110, 4096), (64, 5000), (40, 40), (30, 17), (25, 25), (32, 32),
-                                       (32, 7), (5, 32), (1, 1), (31, 29)])
+                                       (32, 7), (5, 32), (1, 1), (31, 29), (600, 8000), (460, 9001)])
 def test_cpqr_parity(rq, orc, rows, cols):
     rng = np.random.default_rng(rows * cols)
     M = rng.standard_normal((rows, cols)) * np.logspace(0, -4, cols)[rng.permutation(cols)]
