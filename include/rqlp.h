@@ -166,8 +166,10 @@ int rqlp_autorank_ex(rqlp_handle_t h, int64_t m, int64_t n, int b, int l_max, in
 /* Synchronous any-pointer form of rqlp_ex / erqlp_ex / brqlp_ex on handle h: `variant` (2)
  * selects the algorithm (RQLP_VARIANT_*), d (8) is used by ERQLP, b (9) by BRQLP.  A (10), Q (13),
  * T (14), P (15) may be host (pageable or pinned) or device pointers; host operands are copied
- * through device staging buffers inside the call (ldq = m, ldt = l, ldp = n).  Returns after the
- * outputs are written.  This is the end-to-end path bench.py times ("e2e"). */
+ * through device staging buffers inside the call (ldq = m, ldt = l, ldp = n).  A pinned host A is
+ * copied in row panels overlapped with the sketch pass; for BRQLP, pinned host Q and P receive each
+ * block's columns while the later blocks run (the results are bit-identical to the device path).
+ * Returns after the outputs are written.  This is the end-to-end path bench.py times ("e2e"). */
 int rqlp_factorize(rqlp_handle_t h, int variant, int64_t m, int64_t n, int k, int p, int q, int d, int b,
                    const double *A, int64_t lda, uint64_t seed, double *Q, double *T, double *P, int *t_is_upper);
 
