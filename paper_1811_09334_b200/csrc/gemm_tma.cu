@@ -327,6 +327,94 @@ __global__ void __launch_bounds__((NCONS + (FRO ? 1 : 0)) * 32, OCC)
   }
 }
 
+// G = Y^T Y (symmetric, both triangles) for Y m x c with c <= 64 -- the m x 64 Grams of BRQLP's block
+// orthonormalisations.  In the TN kernel the 64 output rows fill half of a 128-row tile (the other
+// half multiplies TMA zero fill).  Here one K-major [8 tn][24] smem tile per stage (the TN kernel's
+// A layout: conflict-free 16-byte fragment loads) feeds BOTH DMMA operands, and only the 8 x 8
+// output tiles on or above the diagonal are formed (36 for c = 64), dealt to the 8 warps.  A CTA
+// sums the k-tiles [blockIdx.x kps, ...) into partial slice blockIdx.x (fixed-order reduce after).
+constexpr int GR_ST = 4, GR_MAXT = 5;   // stages; output tiles per warp (36 / 8 rounded up)
+__global__ void __launch_bounds__(256, 2) gram64_kernel(const __grid_constant__ CUtensorMap mapY, int c,
+                                                        int ktiles_total, int kps, double *__restrict__ C,
+                                                        int64_t ldc, double *__restrict__ part) {
+  const int tn = (c + 7) / 8, ntiles = tn * (tn + 1) / 2;
+  const int TILE = tn * 8 * BK;   // doubles per stage
+  extern __shared__ __align__(128) unsigned char gsm[];
+  double *sY = reinterpret_cast<double *>(gsm);
+  uint64_t *full = reinterpret_cast<uint64_t *>(gsm + (size_t)GR_ST * TILE * 8);
+  uint64_t *empty = full + GR_ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r = lane >> 2, cq = lane & 3;
+  const int kt0 = blockIdx.x * kps;
+  const int nkt = max(0, min(ktiles_total, kt0 + kps) - kt0);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < GR_ST; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int it) {
+    const int st = it % GR_ST;
+    mbar_expect_tx(&full[st], (unsigned)TILE * 8);
+    tma_load_2d(sY + (size_t)st * TILE, &mapY, (kt0 + it) * BK, 0, &full[st]);   // box {BK rows, 8 tn cols}
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapY) : "memory");
+    for (int it = 0; it < GR_ST - 1 && it < nkt; ++it) issue(it);
+  }
+  // this warp's tiles t = warp, warp + 8, ... of the row-major upper triangle (ti <= tj)
+  int ti[GR_MAXT], tj[GR_MAXT];
+#pragma unroll
+  for (int u = 0; u < GR_MAXT; ++u) {
+    int t = warp + 8 * u, a = 0;
+    while (t >= tn - a && a < tn) { t -= tn - a; ++a; }
+    ti[u] = a;
+    tj[u] = a + t;   // (a == tn: past the last tile)
+  }
+  double acc[GR_MAXT][2];
+#pragma unroll
+  for (int u = 0; u < GR_MAXT; ++u) acc[u][0] = acc[u][1] = 0.0;
+  for (int it = 0; it < nkt; ++it) {
+    const int st = it % GR_ST;
+    if (threadIdx.x == 0 && it + GR_ST - 1 < nkt) {
+      if (it >= 1) mbar_wait(&empty[(it - 1) % GR_ST], ((it - 1) / GR_ST) & 1);
+      issue(it + GR_ST - 1);
+    }
+    mbar_wait(&full[st], (it / GR_ST) & 1);
+    const double *y = sY + (size_t)st * TILE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 8; ++kk) {
+#pragma unroll
+      for (int u = 0; u < GR_MAXT; ++u) {
+        if (warp + 8 * u >= ntiles) continue;
+        const double2 av = *reinterpret_cast<const double2 *>(y + (ti[u] * 8 + r) * BK + kk * 8 + 2 * cq);
+        const double2 bv = *reinterpret_cast<const double2 *>(y + (tj[u] * 8 + r) * BK + kk * 8 + 2 * cq);
+        dmma(acc[u][0], acc[u][1], av.x, bv.x);
+        dmma(acc[u][0], acc[u][1], av.y, bv.y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double *dst = part ? part + (size_t)blockIdx.x * c * c : C;
+  const int64_t ld = part ? c : ldc;
+#pragma unroll
+  for (int u = 0; u < GR_MAXT; ++u) {
+    if (warp + 8 * u >= ntiles) continue;
+    const int i = ti[u] * 8 + r;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = tj[u] * 8 + 2 * cq + e;
+      if (i >= c || j >= c) continue;
+      // both triangles (the Cholesky kernel loads the lower one): an off-diagonal tile is mirrored,
+      // a diagonal tile writes its own 8 x 8 entries
+      dst[i + (size_t)j * ld] = acc[u][e];
+      if (ti[u] != tj[u]) dst[j + (size_t)i * ld] = acc[u][e];
+    }
+  }
+}
+
 // Sum of a balanced split's slots: element (i, j) of tile t = (i / BM) ntn + j / bn is the sum,
 // in slot order, of the partial tiles of the CTAs first(t) .. last(t) whose runs touch t.  A CTA
 // reduces a 32 x 32 block (threads along i: coalesced slot reads); the transposed store goes
@@ -781,10 +869,36 @@ bool gemm_tn_tma_bn(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, i
                     int64_t ldv, double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems,
                     const unsigned *cond, unsigned cond_mask, int tri, int bn, double alpha, double beta);
 
+bool gram64(Ctx &c, int64_t m, int64_t cc, const double *Y, int64_t ldy, double *G, int64_t ldg, double *partials,
+            size_t partial_elems) {
+  CUtensorMap my;
+  const int tn = (int)ceil_div(cc, 8);
+  if (!make_map(&my, Y, m, cc, ldy, BK, tn * 8)) return false;
+  const int64_t ktiles = ceil_div(m, BK);
+  // slices: two CTAs per SM when each keeps >= 8 k-tiles, bounded by the partial buffer
+  int64_t S = std::min<int64_t>(2 * c.num_sms, std::max<int64_t>(1, ktiles / 8));
+  if (!partials) S = 1;
+  S = std::min<int64_t>(S, std::max<int64_t>(1, (int64_t)(partial_elems / (size_t)(cc * cc))));
+  const int kps = (int)ceil_div(ktiles, S);
+  S = ceil_div(ktiles, kps);
+  const size_t smem = (size_t)GR_ST * tn * 8 * BK * 8 + 2 * GR_ST * 8;
+  smem_attr((const void *)gram64_kernel, (int)smem);
+  gram64_kernel<<<(unsigned)S, 256, smem, c.stream>>>(my, (int)cc, (int)ktiles, kps, G, ldg, S > 1 ? partials : nullptr);
+  RQLP_LAUNCHED(c);
+  if (S > 1) launch_reduce(c, cc, cc, (int)S, partials, 1.0, 0.0, G, ldg, false, nullptr, 0);
+  return true;
+}
+
 bool gemm_tn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int64_t lda, const double *V, int64_t ldv,
                  double *Z, int64_t ldz, bool trans_out, double *partials, size_t partial_elems, const unsigned *cond,
                  unsigned cond_mask, int tri, double alpha, double beta) {
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
+  // a Gram of 17..64 columns: the dedicated kernel (measured: 262144 x 64 CholeskyQR2 473 -> 321 us,
+  // C4 554.9 -> 551.1 ms; 16 columns: the TN kernel is as fast)
+  static const bool gram_off = env_off("RQLP_GRAM64");   // measurement switch
+  if (tri == 1 && A == V && lda == ldv && k == cc && cc > 16 && cc <= 64 && !cond && !trans_out && alpha == 1.0 &&
+      beta == 0.0 && !gram_off && gram64(c, m, cc, A, lda, Z, ldz, partials, partial_elems))
+    return true;
   const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(m, BK)) : ColSplit();
   if (cs.c1 > 0) {
     CUtensorMap probe;
