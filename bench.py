@@ -317,6 +317,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"])
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="diagnostic (1 GPU): time ONE rank's row block of an N-GPU strong-scaling run through the "
+                         "row-sharded NCCL handle (a world-size-1 communicator: every exchange step is issued, "
+                         "no link time) -- the per-rank compute time behind the projected efficiency in DESIGN.md")
+    ap.add_argument("--shard-plain", action="store_true",
+                    help="with --shard-of: the same row block on the single-GPU handle (graph replay, no exchange "
+                         "steps) -- separates the sharded path's own overhead from the smaller shape's efficiency")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -337,6 +344,19 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
+    elif args.shard_of > 1 and args.shard_plain:
+        args.no_cpu_baseline = True
+    elif args.shard_of > 1:
+        import socket
+
+        import torch.distributed as dist
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        group = dist.group.WORLD
+        args.no_cpu_baseline = True
 
     import paper_1811_09334_b200 as rq
     from paper_1811_09334_b200 import build as rqbuild
@@ -347,9 +367,11 @@ def main():
     from paper_1811_09334_b200.dist import max_over_ranks, row_block
     cg = dataclasses.replace(c, m=c.m * world) if scaling == "weak" else c
     r0, r1 = row_block(cg.m, rank, world)
+    if args.shard_of > 1:   # rank 0's block of an N-rank run
+        r0, r1 = row_block(cg.m, 0, args.shard_of)
     m_loc = r1 - r0
     t0 = time.time()
-    A = make_A_config(cg, device=dev, row_range=(r0, r1) if world > 1 else None)
+    A = make_A_config(cg, device=dev, row_range=(r0, r1) if (world > 1 or args.shard_of > 1) else None)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     log(f"[bench] rank {rank}: A {tuple(A.shape)} (rows {r0}..{r1} of {cg.m}) generated in {time.time() - t0:.1f}s")
@@ -514,6 +536,10 @@ def main():
                 "stages_ms": {k: round(sum(v) / len(v), 4) for k, v in stage_ms.items()},
                 "stages_total_ms": {k: round(sum(v), 4) for k, v in stage_ms.items()},
                 "replicated_outputs_identical": replicated_identical, "device_flags": flags}
+        if args.shard_of > 1:
+            line["shard_of"] = {"n_ranks": args.shard_of, "rows": m_loc, "handle": "single-GPU" if args.shard_plain else "nccl world 1",
+                                "note": "ONE rank's block through the sharded (NCCL, world-size-1) handle; a "
+                                        "diagnostic, not a bench value: roofline_whole_factorisation is meaningless here"}
         print(json.dumps(line), flush=True)
     if group is not None:
         torch.distributed.destroy_process_group()
