@@ -237,6 +237,15 @@ int rqlp_set_timing(rqlp_handle_t h, int enable);
 int rqlp_get_timing(rqlp_handle_t h, const char **names, float *ms, int capacity);
 /* Kernel launches issued by the last call (for bench.py's gpu_launches). */
 int64_t rqlp_launch_count(rqlp_handle_t h);
+/* Row-sharded handles (rqlp_create_dist / rqlp_create_loopback) run each factorisation
+ * optimistically: the orthonormalisations (Alg. 1 l.3) are CholeskyQR2 with no
+ * device-to-host readback; a Cholesky breakdown (a sketch beyond CholeskyQR2's reach) is recorded on
+ * the device, read back once when the factorisation has been enqueued, and the factorisation is then
+ * repeated on the careful path (shifted passes driven from the host, one readback per orth).  Every
+ * rank takes the same decision (the Grams are summed to identical bits).  Returns how many calls on
+ * this handle were repeated so; -1 for an invalid handle.  RQLP_SHARDED_OPTIMISTIC=0 in the
+ * environment selects the careful path from the start. */
+int64_t rqlp_careful_rerun_count(rqlp_handle_t h);
 
 #ifdef __cplusplus
 }

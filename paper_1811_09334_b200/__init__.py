@@ -185,6 +185,11 @@ class Handle:
     def launches(self) -> int:
         return int(lib().rqlp_launch_count(self.h))
 
+    def careful_reruns(self) -> int:
+        """Row-sharded handles: factorisations repeated on the careful path after a Cholesky
+        breakdown in the optimistic run (rqlp_careful_rerun_count)."""
+        return int(lib().rqlp_careful_rerun_count(self.h))
+
     def __del__(self):
         try:
             if getattr(self, "h", None) and self.h.value:

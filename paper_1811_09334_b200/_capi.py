@@ -50,6 +50,7 @@ SIGNATURES = [
     ("rqlp_set_timing", _int, [_vp, _int]),
     ("rqlp_get_timing", _int, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _int]),
     ("rqlp_launch_count", _i64, [_vp]),
+    ("rqlp_careful_rerun_count", _i64, [_vp]),
 ]
 
 _lib = None

@@ -68,6 +68,8 @@ struct rqlp_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> *cur_events = nullptr;
   bool trace_free = getenv("RQLP_ENGINE_TRACE") == nullptr;
+  bool graph_failed = false;      // a sharded capture failed once: eager from then on
+  int64_t careful_reruns = 0;     // optimistic sharded runs that had to be repeated carefully
 };
 
 namespace rqlpk {
@@ -149,32 +151,68 @@ void reset_timing(rqlp_handle_t h) {
   if (h->timing) fill_pool(h->eager_pool);
 }
 
+// Row-sharded handles run optimistically by default: no COND-word readback (stream synchronisation)
+// per orth; a Cholesky breakdown anywhere sets STICKY_WORD, read back ONCE at the end of the
+// factorisation, and the factorisation is then rerun on the careful host-driven path.  Every rank
+// sees the same word (the Grams are summed to identical bits), so the ranks stay in step.
+// RQLP_SHARDED_OPTIMISTIC=0 restores the per-orth readback.
+bool optimistic_enabled(rqlp_handle_t h) {
+  if (!h->comm) return false;
+  const char *e = getenv("RQLP_SHARDED_OPTIMISTIC");
+  return !(e && e[0] == '0');
+}
+
 bool graphs_enabled(rqlp_handle_t h) {
   static int env = -1;
   if (env < 0) {
     const char *e = getenv("RQLP_GRAPHS");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env == 1 && h->comm == nullptr && h->trace_free;
+  if (env != 1 || !h->trace_free) return false;
+  if (h->comm == nullptr) return true;
+  // NCCL handles: graph replay of the optimistic run (ncclAllReduce is capturable) is opt-in
+  // (RQLP_SHARDED_GRAPHS=1): only world size 1 could be exercised on this run's single GPU.  The
+  // loopback ranks take host-side turns inside every sum and cannot be captured.
+  const char *g = getenv("RQLP_SHARDED_GRAPHS");
+  return g && g[0] == '1' && comm_kind(h->comm) == COMM_NCCL && optimistic_enabled(h) && !h->graph_failed;
+}
+
+// After an optimistic run on a sharded handle: one readback; on a recorded breakdown the careful rerun.
+template <typename F>
+void finish_optimistic(rqlp_handle_t h, F &enqueue) {
+  unsigned st = 0;
+  RQLP_CUDA(cudaMemcpyAsync(&st, h->dflags + STICKY_WORD, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+  RQLP_CUDA(cudaStreamSynchronize(h->stream));
+  if (!st) return;
+  Ctx c = make_ctx(h);
+  reset_timing(h);
+  enqueue(c);
+  h->launches += c.launches;
+  h->careful_reruns++;
 }
 
 // Run `enqueue(Ctx&)` eagerly on the handle's stream, or -- from the second call with the same
 // key -- as a CUDA graph captured on a handle-owned stream and replayed on the handle's stream.
 template <typename F>
 int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
+  const bool opt = optimistic_enabled(h);
   if (!graphs_enabled(h)) {
     Ctx c = make_ctx(h);
+    c.optimistic = opt;
     reset_timing(h);
     enqueue(c);
     h->launches = c.launches;
+    if (opt) finish_optimistic(h, enqueue);
     return RQLP_OK;
   }
   auto it = h->graphs.find(key);
   if (it == h->graphs.end() && h->seen[key]++ == 0) {  // first call: eager (also warms static state)
     Ctx c = make_ctx(h);
+    c.optimistic = opt;
     reset_timing(h);
     enqueue(c);
     h->launches = c.launches;
+    if (opt) finish_optimistic(h, enqueue);
     return RQLP_OK;
   }
   if (!h->gstream) {
@@ -188,6 +226,7 @@ int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
     c.events = &e.events;
     c.pool = &e.pool;
     c.capturing = true;
+    c.optimistic = opt;
     cudaGraph_t g = nullptr;
     RQLP_CUDA(cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
     try {
@@ -195,7 +234,18 @@ int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
     } catch (...) {
       cudaStreamEndCapture(h->gstream, &g);
       if (g) cudaGraphDestroy(g);
-      throw;
+      if (!h->comm) throw;
+      // a sharded capture that fails (e.g. a collective library that cannot be captured) falls
+      // back to the eager optimistic run for the rest of the handle's life
+      cudaGetLastError();
+      h->graph_failed = true;
+      Ctx ce = make_ctx(h);
+      ce.optimistic = opt;
+      reset_timing(h);
+      enqueue(ce);
+      h->launches = ce.launches;
+      if (opt) finish_optimistic(h, enqueue);
+      return RQLP_OK;
     }
     RQLP_CUDA(cudaStreamEndCapture(h->gstream, &g));
     cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
@@ -219,6 +269,7 @@ int with_graph(rqlp_handle_t h, const std::string &key, F enqueue) {
   RQLP_CUDA(cudaGraphLaunch(it->second.exec, h->stream));
   h->cur_events = &it->second.events;
   h->launches = it->second.launches;
+  if (opt) finish_optimistic(h, enqueue);
   return RQLP_OK;
 }
 
@@ -1407,6 +1458,7 @@ int rqlp_get_timing(rqlp_handle_t h, const char **names, float *ms, int capacity
 }
 
 int64_t rqlp_launch_count(rqlp_handle_t h) { return valid(h) ? h->launches : -1; }
+int64_t rqlp_careful_rerun_count(rqlp_handle_t h) { return valid(h) ? h->careful_reruns : -1; }
 
 // Debug only (not in rqlp.h): copy the engine phase trace (RQLP_ENGINE_TRACE=1) to the host.
 int rqlp_debug_trace(unsigned long long *host, int count) {

@@ -98,6 +98,7 @@ enum DevFlag : int {
   COND_WORD = 1,       // scratch condition for conditionally executed kernels
   BAR_COUNT = 2,       // cooperative grid barrier (count, generation)
   BAR_GEN = 3,
+  STICKY_WORD = 4,     // row-sharded optimistic run: set when any orth took a shifted pass (-> careful rerun)
   NUM_DEV_FLAGS = 8
 };
 
@@ -114,6 +115,9 @@ struct Ctx {
   std::vector<cudaEvent_t> *pool = nullptr;  // pre-created events (no cudaEventCreate under capture)
   size_t pool_next = 0;
   bool capturing = false;
+  // row-sharded runs only: the rare orth branch is not taken on the host (no COND-word readback per
+  // orth); a breakdown only sets STICKY_WORD and the caller reruns the factorisation carefully
+  bool optimistic = false;
   void mark(const char *name);
   // row-sharded runs (comm.cu): NCCL communicator, rank, number of ranks
   void *comm = nullptr;

@@ -629,6 +629,9 @@ static void cholqr_pass(Ctx &c, OrthScratch &s, int64_t m, int64_t n, const doub
 }
 
 __global__ void or_flag_kernel(unsigned *word, unsigned bits) { atomicOr(word, bits); }
+__global__ void sticky_kernel(const unsigned *cond, unsigned mask, unsigned *sticky) {
+  if (*cond & mask) *sticky = 1u;
+}
 
 // The rare branch for row-sharded orth (orth_rescue.cu's algorithm with allreduced Grams, driven
 // from the host): if the COND word holds one of `mask`'s bits, CholeskyQR passes (shifted on
@@ -638,6 +641,13 @@ __global__ void or_flag_kernel(unsigned *word, unsigned bits) { atomicOr(word, b
 static void sharded_rescue(Ctx &c, OrthScratch &s, int64_t m, int64_t n, double *V, int64_t ldv, const double *Y,
                            int64_t ldy, double *R, int64_t ldr, unsigned mask) {
   unsigned *condw = c.dflags + COND_WORD;
+  if (c.optimistic) {
+    // no readback: remember that this orth broke down; with_graph() reads the sticky word once at
+    // the end of the factorisation and reruns it on the careful (host-driven) path
+    sticky_kernel<<<1, 1, 0, c.stream>>>(condw, mask, c.dflags + STICKY_WORD);
+    RQLP_LAUNCHED(c);
+    return;
+  }
   unsigned host = 0;
   RQLP_CUDA(cudaMemcpyAsync(&host, condw, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
   RQLP_CUDA(cudaStreamSynchronize(c.stream));

@@ -53,6 +53,32 @@ def test_nccl_world1_bit_identical(world1, variant):
     torch.cuda.synchronize()
     for key in ("Q", "T", "P", "piv0"):
         assert torch.equal(g0[key], g1[key]), key
+    assert hd.careful_reruns() == 0
+
+
+@pytest.mark.parametrize("variant", ["erqlp", "brqlp"])
+def test_nccl_world1_graph_replay(world1, variant, monkeypatch):
+    """RQLP_SHARDED_GRAPHS=1 (opt-in): the optimistic sharded run, ncclAllReduce calls included, is
+    captured on the second call and replayed from the third; every call returns the bits of the
+    single-GPU handle, and a sketch that breaks CholeskyQR2 still ends on the careful path."""
+    dist = world1
+    import paper_1811_09334_b200 as rq
+    monkeypatch.setenv("RQLP_SHARDED_GRAPHS", "1")
+    rng = np.random.default_rng(4)
+    U, _ = np.linalg.qr(rng.standard_normal((1500, 200)))
+    V, _ = np.linalg.qr(rng.standard_normal((600, 200)))
+    A = torch.from_numpy(np.ascontiguousarray(((U * np.arange(1, 201.0) ** -1.2) @ V.T).T)).cuda().t()
+    kw = dict(erqlp=dict(q=1, d=2), brqlp=dict(q=1, b=16))[variant]
+    g0 = rq.factorize(A, 40, 8, seed=5, handle=rq.Handle(), **kw)
+    hd = rq.Handle(group=dist.group.WORLD)
+    g1 = None
+    for _ in range(4):       # eager, capture + replay, replay, replay (the freed outputs are handed out
+        g1 = None            # again by the caching allocator: same pointers, same graph key)
+        g1 = rq.factorize(A, 40, 8, seed=5, handle=hd, **kw)
+        torch.cuda.synchronize()
+        for key in ("Q", "T", "P", "piv0"):
+            assert torch.equal(g0[key], g1[key]), key
+    assert hd.careful_reruns() == 0
 
 
 @pytest.mark.parametrize("kind", ["illcond", "deficient", "zero"])
@@ -76,6 +102,7 @@ def test_nccl_world1_rare_branch(world1, kind, d):
     hd = rq.Handle(group=dist.group.WORLD)
     g1 = rq.factorize(A, 12, 4, q=1, d=d, seed=5, handle=hd)
     flags = hd.sync()
+    assert hd.careful_reruns() == 1   # the optimistic run recorded the breakdown -> careful rerun
     g0 = rq.factorize(A, 12, 4, q=1, d=d, seed=5, handle=rq.Handle())
     torch.cuda.synchronize()
     Q1, T1, P1 = (np.asfortranarray(g1[k].cpu().numpy()) for k in ("Q", "T", "P"))
@@ -88,3 +115,30 @@ def test_nccl_world1_rare_branch(world1, kind, d):
     k = len(sig) if kind != "illcond" else 6
     if kind != "zero":
         np.testing.assert_allclose(np.abs(np.diag(T1))[:k], np.abs(np.diag(T0))[:k], rtol=1e-8)
+
+
+def test_nccl_world1_graph_replay_rare_branch(world1, monkeypatch):
+    """With RQLP_SHARDED_GRAPHS=1 a sketch beyond CholeskyQR2's reach sets the sticky word in the
+    eager run AND in every replay: each call is repeated on the careful path and returns the same
+    bits as the careful path from the start."""
+    dist = world1
+    import paper_1811_09334_b200 as rq
+    rng = np.random.default_rng(11)
+    sig = np.logspace(0, -13, 16)
+    U, _ = np.linalg.qr(rng.standard_normal((600, 16)))
+    V, _ = np.linalg.qr(rng.standard_normal((400, 16)))
+    A = torch.from_numpy(np.ascontiguousarray(((U * sig) @ V.T).T)).cuda().t()
+    monkeypatch.setenv("RQLP_SHARDED_OPTIMISTIC", "0")
+    ref = rq.factorize(A, 12, 4, q=1, d=2, seed=5, handle=rq.Handle(group=dist.group.WORLD))
+    torch.cuda.synchronize()
+    monkeypatch.setenv("RQLP_SHARDED_OPTIMISTIC", "1")
+    monkeypatch.setenv("RQLP_SHARDED_GRAPHS", "1")
+    hd = rq.Handle(group=dist.group.WORLD)
+    g1 = None
+    for i in range(3):
+        g1 = None
+        g1 = rq.factorize(A, 12, 4, q=1, d=2, seed=5, handle=hd)
+        assert hd.sync() & 1
+        assert hd.careful_reruns() == i + 1
+        for key in ("Q", "T", "P", "piv0"):
+            assert torch.equal(ref[key], g1[key]), key
