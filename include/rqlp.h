@@ -65,7 +65,9 @@ int rqlp_create(rqlp_handle_t *h, int device, void *cuda_stream);
  * to the 128-byte ncclUniqueId created by rank 0 and shared by the caller (e.g. through
  * torch.distributed).  Every rank then calls the factorisations collectively with its local
  * row count m_local, its row block of A and the same seed; Q is returned for the local rows,
- * L, P and the pivots are replicated. */
+ * L, P and the pivots are replicated.  Unlike the single-GPU handle, a factorisation call on a
+ * sharded handle synchronises its stream once before returning (the breakdown word of the
+ * optimistic run, see rqlp_careful_rerun_count). */
 int rqlp_create_dist(rqlp_handle_t *h, int device, void *cuda_stream, const void *nccl_unique_id,
                      int rank, int nranks);
 int rqlp_get_unique_id(void *nccl_unique_id_out /* 128 bytes */);
