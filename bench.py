@@ -102,7 +102,11 @@ class ClockSampler:
                 sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                 bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 rs = [nm for nm, attr in self.REASONS if bits & getattr(nv, attr, 0)]
-                self.samples.append((time.perf_counter(), sm, rs))
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pw = None
+                self.samples.append((time.perf_counter(), sm, rs, pw))
             except Exception:
                 pass
             time.sleep(0.002)
@@ -131,7 +135,7 @@ class ClockSampler:
     def __exit__(self, *exc):
         self.t1 = time.perf_counter()
         if self.thread is not None:
-            while not any(t >= self.t0 for t, _, _ in self.samples):
+            while not any(s[0] >= self.t0 for s in self.samples):
                 time.sleep(0.001)
             self.stop = True
             self.thread.join(timeout=1)
@@ -149,9 +153,15 @@ class ClockSampler:
             inside = [s for s in self.samples if self.t0 <= s[0] <= self.t1]
             if not inside:
                 inside = [min((s for s in self.samples if s[0] >= self.t0), key=lambda s: s[0])]
-            reasons = sorted({r for _, _, rs in inside for r in rs})
-            return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": self.mx,
-                    "reasons": reasons, "samples": len(inside), "source": "nvml"}
+            reasons = sorted({r for s in inside for r in s[2]})
+            mhz = sorted(s[1] for s in inside)
+            pws = [s[3] for s in inside if s[3] is not None]
+            return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.mx,
+                    "reasons": reasons, "samples": len(inside), "source": "nvml",
+                    "sm_mhz_min": mhz[0], "sm_mhz_p05": mhz[len(mhz) // 20],
+                    "power_cap_sample_frac": round(sum(1 for s in inside if "sw_power_cap" in s[2]) / len(inside), 4),
+                    "power_w_mean": round(sum(pws) / len(pws), 1) if pws else None,
+                    "power_w_max": round(max(pws), 1) if pws else None}
         sms, mx, reasons = [], None, set()
         names = [nm for nm, _ in self.REASONS]
         for line in (self.out or "").splitlines():

@@ -582,7 +582,12 @@ ColSplit choose_colsplit(int64_t cc, int64_t ktiles) {
     for (int b2 : kBNs) {
       if (b2 < rem || (b2 < 64 && rem > 64)) continue;
       const int64_t pad = b2 - rem;
-      if (pad < best_pad || (pad == best_pad && best.c1 > 0 && b1 > best.bn1)) {
+      // equal padding: the wider first width.  RQLP_COLSPLIT_PREFER=w (measurement switch) puts width w
+      // first: C4's sketch as 3 x 128 + 144 instead of 3 x 144 + 96 measured the same inside the
+      // power-capped step (128.6 / 130.8 ms against 129.2 / 130.1 ms)
+      static const int prefer = [] { const char *e = getenv("RQLP_COLSPLIT_PREFER"); return e ? atoi(e) : 0; }();
+      auto rank = [&](int b) { return b == prefer ? 1000 : b; };
+      if (pad < best_pad || (pad == best_pad && best.c1 > 0 && rank(b1) > rank(best.bn1))) {
         best_pad = pad;
         best.c1 = c1;
         best.bn1 = b1;
@@ -796,6 +801,17 @@ bool gemm_nn_tma(Ctx &c, int64_t m, int64_t cc, int64_t k, const double *A, int6
   if (tma_disabled() || m < 1 || cc < 1 || k < 1) return false;
   static const bool fro_off = env_off("RQLP_FRO_FUSED");   // measurement switch: separate ||A||^2 pass
   if (fro && (cond || tri || fro_off)) return false;
+  // measurement switch RQLP_NN_SLAB=w: a wide long-K pass as column slabs of w (one launch each)
+  static const int slab = [] { const char *e = getenv("RQLP_NN_SLAB"); return e ? atoi(e) : 0; }();
+  if (slab >= 16 && !fro && tri == 0 && !cond && cc > slab && ceil_div(k, BK) > 16) {
+    for (int64_t c0 = 0; c0 < cc; c0 += slab) {
+      const int64_t w = std::min<int64_t>(slab, cc - c0);
+      if (!gemm_nn_tma(c, m, w, k, A, lda, X + c0 * ldx, ldx, Y + c0 * ldy, ldy, partials, partial_elems, nullptr, 0,
+                       0, nullptr, alpha, beta))
+        throw CudaError("gemm_nn_tma: slab not launchable");
+    }
+    return true;
+  }
   const ColSplit cs = tri == 0 ? choose_colsplit(cc, ceil_div(k, BK)) : ColSplit();
   if (cs.c1 > 0) {
     // the ||A||^2 goes with one column range (each reads all of A), one whose width can carry it
