@@ -620,8 +620,9 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);        // C = V_<j^T V_j
     allreduce_sum(c, P.C, LL * bj);
     gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems);  // V_j -= V_<j C
-    launch_copy(c, m, bj, Vj, ldm, P.Qt2, ldm, false);
-    orth(c, P.orth, m, bj, P.Qt2, ldm, Vj, ldm, nullptr, 0, sh);                            // CholeskyQR2
+    // CholeskyQR2 in place: pass 1 reads V_j into the orth scratch, pass 2 writes V_j (no R asked, so
+    // nothing reads the input again)
+    orth(c, P.orth, m, bj, Vj, ldm, Vj, ldm, nullptr, 0, sh);
   };
   // q = 0 (NEXT-4): the range finder needs no A-pass per block, so every V_j is built first
   // and ONE batched pass B = V^T A replaces the h per-block projections; the deflation
@@ -695,7 +696,9 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     }
     if (c0 > 0) {
       const int64_t lde = round_up(b, 8);
-      gemm_tn(c, m, c0, bj, Vj, ldm, P.V, ldm, P.D, lde, false, P.part, P.part_elems);   // E = Vj^T V_<j (bj x c0)
+      // E = Vj^T V_<j (bj x c0), formed as (V_<j^T V_j)^T: c0 output rows fill the kernel's 128-row
+      // tiles, bj = 64 rows left half of each tile as zero fill (C4, c0 = 384: 745 -> 389 us)
+      gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.D, lde, true, P.part, P.part_elems);
       allreduce_sum(c, P.D, lde * c0);
       gemm_nn_ab(c, bj, n, c0, -1.0, P.D, lde, B, LL, 1.0, Bj, ldbj, P.part, P.part_elems);   // B_j -= E B_<j
     }
