@@ -606,10 +606,18 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
   // and R_ii > 0, so P(Y_j R^-1) = (P Y_j) R^-1 spans the same space with the same R_ii > 0
   // normalisation.  3 CholeskyQR passes where the literal form takes 6 (C4: 12 -> 6 m x b passes
   // per block).  The first block has nothing to project against: V_1 = qr(Y_1).
-  auto block_orth = [&](double *Yj, int64_t c0, int64_t bj) {
+  // span_only (the V_j that only feeds a power step, q >= 1): the deflated product
+  // Z = A^(j-1)^T V_j = A^T V_j - B_<j^T (V_<j^T V_j) depends on V_j only through the span of its
+  // component outside span(V_<j) -- A^(j-1) annihilates span(V_<j) and the V_<j^T V_j term is formed
+  // explicitly -- so the first projection and ONE CholeskyQR pass (W R^-1 spans (I - P) Y_j) suffice,
+  // as for RQLP's intermediate bases (orth's span_only); the block's final V_j gets the full sequence.
+  // RQLP_BRQLP_PRE_SPAN=0: the full sequence there too (measurement switch).
+  static const bool pre_span = [] { const char *e = getenv("RQLP_BRQLP_PRE_SPAN"); return !(e && e[0] == '0'); }();
+  auto block_orth = [&](double *Yj, int64_t c0, int64_t bj, bool span_only = false) {
     double *Vj = P.V + c0 * ldm;
+    span_only = span_only && pre_span;
     if (c0 == 0) {
-      orth(c, P.orth, m, bj, Yj, ldm, Vj, ldm, nullptr, 0, sh);
+      orth(c, P.orth, m, bj, Yj, ldm, Vj, ldm, nullptr, 0, sh, span_only);
       return;
     }
     c.mark("b_other");
@@ -617,6 +625,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     allreduce_sum(c, P.C, LL * bj);
     gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Yj, ldm, P.part, P.part_elems);  // W = Y_j - V_<j C
     orth(c, P.orth, m, bj, Yj, ldm, Vj, ldm, nullptr, 0, sh, true);                         // span of W
+    if (span_only) return;
     gemm_tn(c, m, bj, c0, P.V, ldm, Vj, ldm, P.C, LL, false, P.part, P.part_elems);        // C = V_<j^T V_j
     allreduce_sum(c, P.C, LL * bj);
     gemm_nn_ab(c, m, bj, c0, -1.0, P.V, ldm, P.C, LL, 1.0, Vj, ldm, P.part, P.part_elems);  // V_j -= V_<j C
@@ -652,7 +661,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
       c.mark("pass_block_sketch");
     }
     if (!two_pass) {
-      block_orth(P.Y + c0 * ldm, c0, bj);                                                  // l.4-5
+      block_orth(P.Y + c0 * ldm, c0, bj, q > 0);                                           // l.4-5
       for (int it = 0; it < q; ++it) {                                                     // deflated power step (R16)
         if (h->dbgVP) launch_copy(c, m, bj, Vj, ldm, h->dbgVP + (it * l + c0) * h->ldVP, h->ldVP, false);
         c.mark("b_other");
