@@ -674,7 +674,9 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
           gemm_tn_ab(c, c0, bj, n, -1.0, B, LL, P.C, LL, 1.0, P.Z, ldn, P.part, P.part_elems);   // Z -= B_<j^T C
         }
         if (h->dbgZ) launch_copy(c, n, bj, P.Z, ldn, h->dbgZ + (it * l + c0) * h->ldZ, h->ldZ, false);
-        orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false);                     // W = qr(Z)
+        // W = qr(Z): only span(W) reaches Y = A^(j-1) W and the block's V_j, so one CholeskyQR pass
+        // (orth's span_only, as in RQLP's power steps)
+        orth(c, P.orth, n, bj, P.Z, ldn, P.W, ldn, nullptr, 0, false, pre_span);
         if (h->dbgW) launch_copy(c, n, bj, P.W, ldn, h->dbgW + (it * l + c0) * h->ldW, h->ldW, false);
         c.mark("b_other");
         if (fro_late && j == h_blocks - 1 && it == 0) {   // Y = A W, with ||A||_F^2 (see above)
