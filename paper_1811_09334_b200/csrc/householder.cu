@@ -18,6 +18,8 @@
 // double-buffered by step parity, so a CTA can run at most one step ahead without overwriting
 // data a slower CTA still reads.  Every CTA recomputes the reflector from the winner's column
 // with the same fixed-order reduction, so all hold bit-identical v, tau; CTA 0 stores it.
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace rqlpk {
@@ -390,29 +392,40 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : GT) : 1024, 1) hh_engine
             }
           } else if (len <= 1 + 32 * RPL) {
             // columns in global memory, short enough to stay in registers for the step: one read
-            // and one write of the column (all loads in flight) instead of read, read, write
-            double reg[RPL];
+            // and one write of the column (all loads in flight) instead of read, read, write.
+            // The unrolled row loops are sized to the rows left (8, 16, 24, 32 or 40 per lane): late in
+            // the factorisation a fixed 40-iteration loop issued mostly predicated-off instructions
+            // (same operations on the same values in the same order: bit-identical results).
+            auto upd = [&](auto rp) {
+              constexpr int RP = decltype(rp)::value;
+              double reg[RP];
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-              const int r = 1 + l8 + 32 * i;
-              reg[i] = r < len ? col[r] : 0.0;
-            }
-            double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;
+              for (int i = 0; i < RP; ++i) {
+                const int r = 1 + l8 + 32 * i;
+                reg[i] = r < len ? col[r] : 0.0;
+              }
+              double w0 = l8 == 0 ? x : 0.0, w1 = 0.0;
 #pragma unroll
-            for (int i = 0; i < RPL; i += 2) {
-              const int r = 1 + l8 + 32 * i;
-              if (r < len) w0 = fma(cp[r] * scal, reg[i], w0);
-              if (i + 1 < RPL && r + 32 < len) w1 = fma(cp[r + 32] * scal, reg[i + 1], w1);
-            }
-            double w = gsum(w0 + w1);
-            w *= tau;
-            x -= w;  // the updated row-j entry (identical in the lanes)
-            if (l8 == 0) col[0] = x;
+              for (int i = 0; i < RP; i += 2) {
+                const int r = 1 + l8 + 32 * i;
+                if (r < len) w0 = fma(cp[r] * scal, reg[i], w0);
+                if (i + 1 < RP && r + 32 < len) w1 = fma(cp[r + 32] * scal, reg[i + 1], w1);
+              }
+              double w = gsum(w0 + w1);
+              w *= tau;
+              x -= w;  // the updated row-j entry (identical in the lanes)
+              if (l8 == 0) col[0] = x;
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-              const int r = 1 + l8 + 32 * i;
-              if (r < len) col[r] = fma(-w, cp[r] * scal, reg[i]);
-            }
+              for (int i = 0; i < RP; ++i) {
+                const int r = 1 + l8 + 32 * i;
+                if (r < len) col[r] = fma(-w, cp[r] * scal, reg[i]);
+              }
+            };
+            if (len <= 1 + 32 * 8) upd(std::integral_constant<int, 8>{});
+            else if (len <= 1 + 32 * 16) upd(std::integral_constant<int, 16>{});
+            else if (len <= 1 + 32 * 24) upd(std::integral_constant<int, 24>{});
+            else if (len <= 1 + 32 * 32) upd(std::integral_constant<int, 32>{});
+            else upd(std::integral_constant<int, RPL>{});
           } else {
             // longer columns in global memory (L2): a simple strided loop the compiler unrolls, so
             // many loads are in flight
