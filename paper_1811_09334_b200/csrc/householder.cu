@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : GT) : 1024, 1) hh_engine
           } else if (len <= 1 + 32 * RPL) {
             // columns in global memory, short enough to stay in registers for the step: one read
             // and one write of the column (all loads in flight) instead of read, read, write.
-            // The unrolled row loops are sized to the rows left (8, 16, 24, 32 or 40 per lane): late in
+            // The unrolled row loops are sized to the rows left (4, 8, ..., 40 per lane): late in
             // the factorisation a fixed 40-iteration loop issued mostly predicated-off instructions
             // (same operations on the same values in the same order: bit-identical results).
             auto upd = [&](auto rp) {
@@ -421,10 +421,20 @@ __global__ void __launch_bounds__(GRID ? (SMEMC ? 512 : GT) : 1024, 1) hh_engine
                 if (r < len) col[r] = fma(-w, cp[r] * scal, reg[i]);
               }
             };
-            if (len <= 1 + 32 * 8) upd(std::integral_constant<int, 8>{});
-            else if (len <= 1 + 32 * 16) upd(std::integral_constant<int, 16>{});
-            else if (len <= 1 + 32 * 24) upd(std::integral_constant<int, 24>{});
-            else if (len <= 1 + 32 * 32) upd(std::integral_constant<int, 32>{});
+            // (a binary decision tree over rows-per-lane sizes 4, 8, ..., 40)
+            const int need = (len - 1 + 31) >> 5;   // rows per lane below row j
+            if (need <= 20) {
+              if (need <= 8) {
+                if (need <= 4) upd(std::integral_constant<int, 4>{});
+                else upd(std::integral_constant<int, 8>{});
+              } else if (need <= 12) upd(std::integral_constant<int, 12>{});
+              else if (need <= 16) upd(std::integral_constant<int, 16>{});
+              else upd(std::integral_constant<int, 20>{});
+            } else if (need <= 28) {
+              if (need <= 24) upd(std::integral_constant<int, 24>{});
+              else upd(std::integral_constant<int, 28>{});
+            } else if (need <= 32) upd(std::integral_constant<int, 32>{});
+            else if (need <= 36) upd(std::integral_constant<int, 36>{});
             else upd(std::integral_constant<int, RPL>{});
           } else {
             // longer columns in global memory (L2): a simple strided loop the compiler unrolls, so
