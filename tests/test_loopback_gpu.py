@@ -161,6 +161,29 @@ def test_loopback_rare_branch(rq, orc, kind, mode, monkeypatch):
     assert r_g <= 10 * r_o + 1e-13 * max(np.linalg.norm(A), 1.0)
 
 
+@pytest.mark.parametrize("mode", ["optimistic", "careful"])
+def test_loopback_rare_branch_brqlp(rq, orc, mode, monkeypatch):
+    """BRQLP on a rank-6 matrix with l = 24 in blocks of 8 on 2 ranks: the blocks beyond rank(A) are
+    rounding noise, their sketches break CholeskyQR2 -- the optimistic run must notice on every rank,
+    the careful rerun must return an orthonormal Q (reading R28) and the oracle's residual."""
+    monkeypatch.setenv("RQLP_SHARDED_OPTIMISTIC", "1" if mode == "optimistic" else "0")
+    rng = np.random.default_rng(21)
+    m, n = 700, 300
+    sig = np.array([3.0, 2.0, 1.0, 0.5, 0.25, 0.125])
+    A = _rand_A(rng, m, n, sig)
+    out, flags = run_ranks(rq, A, 2, lambda r, Ab, h: rq.factorize(Ab, 20, 4, q=1, b=8, seed=5, handle=h))
+    _replicated_equal(out, ("T", "P", "piv0", "piv1"))
+    assert len(set(flags)) == 1 and flags[0] & 1, flags
+    assert run_ranks.reruns == [1 if mode == "optimistic" else 0] * 2, run_ranks.reruns
+    g = _gather(out)
+    Q, T, P = (np.asfortranarray(g[k].cpu().numpy()) for k in ("Q", "T", "P"))
+    assert np.abs(Q.T @ Q - np.eye(24)).max() <= 1e-13 * 24
+    o = orc.brqlp(A, 20, 4, b=8, q=1, seed=5)
+    r_g, r_o = orc.residual(A, Q, T, P), orc.residual(A, o["Q"], o["T"], o["P"])
+    assert r_g <= 10 * r_o + 1e-13 * np.linalg.norm(A)
+    np.testing.assert_allclose(np.abs(np.diag(T))[:6], np.abs(np.diag(o["T"]))[:6], rtol=1e-8)
+
+
 def test_loopback_host_buffers(rq, orc):
     """rqlp_factorize (the e2e entry point) on loopback ranks with pinned host row blocks."""
     rng = np.random.default_rng(5)
