@@ -55,6 +55,13 @@ extern "C" {
                                         <= 1e-15 of its Gram diagonal, i.e. a direction below
                                         ~3e-8 relative) or a basis column was completed */
 
+#define RQLP_FLAG_REPLICA_MISMATCH 4u /* row-sharded handles: after the sum of the projected B (Alg. 1
+                                        l.4) the ranks did not all hold the same bits
+                                        (a 64-bit hash of B is compared across the ranks); the
+                                        replicated tail may then have diverged -- L, P and the pivots
+                                        are not trustworthy.  Set on every rank.
+                                        RQLP_REPLICA_CHECK=0 in the environment skips the check. */
+
 typedef struct rqlp_handle_s *rqlp_handle_t;
 
 /* Create a single-GPU handle on `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL =

@@ -488,6 +488,7 @@ void range_and_project(Ctx &c, Plan &P, int64_t m, int64_t n, int64_t l, int q, 
   }
   gemm_tn(c, m, l, n, A, lda, P.V, P.ldm, P.B, P.ldl, true, P.part, P.part_elems);    // l.4 B = V^T A
   allreduce_sum(c, P.B, P.ldl * n);
+  check_replicated(c, P.B, P.ldl * n);
   c.mark("pass_project");
   fro2_accumulate(c, l, n, P.B, P.ldl, P.fro_slots, c.dind + 1, true);   // ||B||_F^2 (replicated B)
   if (h->dbgV) launch_copy(c, m, l, P.V, P.ldm, h->dbgV, h->ldV, false);
@@ -645,6 +646,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     c.mark("b_other");
     gemm_tn(c, m, l, n, A, lda, P.V, ldm, B, LL, true, P.part, P.part_elems);           // all V_j^T A
     allreduce_sum(c, B, LL * n);
+    check_replicated(c, B, LL * n);
     c.mark("pass_project");
   }
   for (int64_t j = 0; j < h_blocks; ++j) {
@@ -703,6 +705,7 @@ void enqueue_brqlp(Ctx &c, rqlp_handle_t h, int64_t m, int64_t n, int k, int p, 
     } else {
       gemm_tn(c, m, bj, n, A, lda, Vj, ldm, Bj, ldbj, true, P.part, P.part_elems);
       allreduce_sum(c, Bj, ldbj * n);
+      check_replicated(c, Bj, ldbj * n);
       c.mark("pass_block_project");
     }
     if (c0 > 0) {
@@ -825,8 +828,8 @@ int rqlp_create(rqlp_handle_t *out, int device, void *cuda_stream) {
   cudaSetDevice(device);
   cudaError_t e = cudaMalloc(&h->dflags, NUM_DEV_FLAGS * sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(h->dflags, 0, NUM_DEV_FLAGS * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMalloc(&h->dind, 4 * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(h->dind, 0, 4 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&h->dind, 16 * sizeof(double));   // [0..1] eq. (3); [4..10] replica check
+  if (e == cudaSuccess) e = cudaMemset(h->dind, 0, 16 * sizeof(double));
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     delete h;

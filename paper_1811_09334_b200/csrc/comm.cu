@@ -286,4 +286,55 @@ void allreduce_sum(Ctx &c, double *buf, int64_t count) {
   c.collectives++;
 }
 
+// ---- replica check ------------------------------------------------------------------------
+// The replicated steps (the whole tail) rely on every rank holding the SAME bits of the summed B.
+// After such a sum: a 64-bit hash of the buffer (commutative integer sum of per-element mixes, so the
+// atomics' order does not matter), split into three 22-bit integers held exactly in doubles; their
+// sum over ranks must equal nranks x the rank's own parts, else some rank holds different bits and
+// every rank sets RQLP_FLAG_REPLICA_MISMATCH.  Scratch: dind[4] (the hash), [5..7] own, [8..10] summed.
+__global__ void rep_hash_kernel(const double *__restrict__ buf, int64_t count, unsigned long long *hash) {
+  unsigned long long acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long x = (unsigned long long)__double_as_longlong(buf[i]) + 0x9e3779b97f4a7c15ULL * (unsigned long long)(i + 1);
+    x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27; x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    acc += x;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(hash, acc);
+}
+__global__ void rep_split_kernel(const unsigned long long *hash, double *own, double *sum, int flip) {
+  unsigned long long hv = *hash ^ (flip ? 1ULL : 0ULL);   // flip: debug (a rank pretending to hold other bits)
+  for (int k = 0; k < 3; ++k) {
+    const double v = (double)((hv >> (22 * k)) & (k == 2 ? 0xfffffULL : 0x3fffffULL));
+    own[k] = v;
+    sum[k] = v;
+  }
+}
+__global__ void rep_verify_kernel(const double *own, const double *sum, int nranks, unsigned *flag_word, unsigned bit) {
+  bool ok = true;
+  for (int k = 0; k < 3; ++k) ok = ok && sum[k] == own[k] * (double)nranks;
+  if (!ok) atomicOr(flag_word, bit);
+}
+
+void check_replicated(Ctx &c, const double *buf, int64_t count) {
+  if (!c.comm || count <= 0 || !c.dind) return;
+  const char *eo = getenv("RQLP_REPLICA_CHECK");   // (read per call: a few per factorisation)
+  if (eo && eo[0] == '0') return;
+  const char *ef = getenv("RQLP_DEBUG_REPLICA_FLIP");   // debug: this rank pretends to hold other bits
+  const int flip_rank = ef ? atoi(ef) : -1;
+  unsigned long long *hash = reinterpret_cast<unsigned long long *>(c.dind + 4);
+  double *own = c.dind + 5, *sum = c.dind + 8;
+  RQLP_CUDA(cudaMemsetAsync(hash, 0, sizeof(unsigned long long), c.stream));
+  const int64_t blocks = std::min<int64_t>(ceil_div(count, 256 * 4), 148 * 4);
+  rep_hash_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, c.stream>>>(buf, count, hash);
+  RQLP_LAUNCHED(c);
+  rep_split_kernel<<<1, 1, 0, c.stream>>>(hash, own, sum, c.rank == flip_rank ? 1 : 0);
+  RQLP_LAUNCHED(c);
+  allreduce_sum(c, sum, 3);
+  rep_verify_kernel<<<1, 1, 0, c.stream>>>(own, sum, c.nranks, c.dflags + FLAG_WORD, 4u /* RQLP_FLAG_REPLICA_MISMATCH */);
+  RQLP_LAUNCHED(c);
+}
+
 }  // namespace rqlpk

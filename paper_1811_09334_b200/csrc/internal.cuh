@@ -160,6 +160,9 @@ int comm_async_error(void *comm);
 void comm_call_begin(void *comm);
 void comm_call_end(void *comm, bool failed);
 void allreduce_sum(Ctx &c, double *buf, int64_t count);
+// after a sum whose result every rank must hold bit-identically (the replicated B): verify it across
+// the ranks, RQLP_FLAG_REPLICA_MISMATCH on every rank otherwise (comm.cu)
+void check_replicated(Ctx &c, const double *buf, int64_t count);
 
 // Bump allocator over a workspace; base == nullptr measures only.
 struct Arena {

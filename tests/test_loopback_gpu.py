@@ -184,6 +184,23 @@ def test_loopback_rare_branch_brqlp(rq, orc, mode, monkeypatch):
     np.testing.assert_allclose(np.abs(np.diag(T))[:6], np.abs(np.diag(o["T"]))[:6], rtol=1e-8)
 
 
+@pytest.mark.parametrize("variant", ["erqlp", "brqlp", "brqlp_q0"])
+def test_loopback_replica_mismatch_is_flagged(rq, variant, monkeypatch):
+    """The replicated tail relies on every rank holding the same bits of the summed B; the library
+    compares a hash of B across the ranks after the sum.  With one rank pretending to hold other bits
+    (RQLP_DEBUG_REPLICA_FLIP) EVERY rank must report RQLP_FLAG_REPLICA_MISMATCH (4); without it none
+    does (the other loopback tests assert flags == 0)."""
+    rng = np.random.default_rng(8)
+    A = _rand_A(rng, 600, 300, np.arange(1, 201.0) ** -1.5)
+    kw = dict(erqlp=dict(q=1, d=2), brqlp=dict(q=1, b=8), brqlp_q0=dict(q=0, b=8))[variant]
+    monkeypatch.setenv("RQLP_DEBUG_REPLICA_FLIP", "1")
+    _, flags = run_ranks(rq, A, 3, lambda r, Ab, h: rq.factorize(Ab, 20, 4, seed=5, handle=h, **kw))
+    assert all(f & 4 for f in flags), flags
+    monkeypatch.delenv("RQLP_DEBUG_REPLICA_FLIP")
+    _, flags = run_ranks(rq, A, 3, lambda r, Ab, h: rq.factorize(Ab, 20, 4, seed=5, handle=h, **kw))
+    assert all(f == 0 for f in flags), flags
+
+
 def test_loopback_host_buffers(rq, orc):
     """rqlp_factorize (the e2e entry point) on loopback ranks with pinned host row blocks."""
     rng = np.random.default_rng(5)
